@@ -1,0 +1,70 @@
+"""Build libtrg.so in-tree for sm_100a (B200).
+
+    python -m paper_1901_01652_b200.build        (or __graft_entry__.build())
+
+Each CUDA / C++ source is compiled by nvcc with
+``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` and linked into
+paper_1901_01652_b200/libtrg.so (git-ignored, travels to the GPU box with
+gpurun). Objects are rebuilt only when a source or header is newer.
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libtrg.so")
+
+SOURCES = ["sketch.cu", "ttm.cu", "qr.cu", "tr.cu", "runtime.cpp", "host_solve.cpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _flags():
+    return ARCH + [
+        "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+        "-Xcompiler", "-fPIC,-fopenmp,-O3",
+        "-Xptxas", "-v" if os.environ.get("TRG_PTXAS_VERBOSE") else "-O3",
+        "-ccbin", "g++",
+        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+    ]
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".hpp", ".cuh"))]
+    return hs + [os.path.join(ROOT, "include", "trg.h")]
+
+
+def _newer(src, dst, deps):
+    if not os.path.exists(dst):
+        return True
+    t = os.path.getmtime(dst)
+    return any(os.path.getmtime(p) > t for p in [src] + deps)
+
+
+def build(verbose=False):
+    os.makedirs(BUILD, exist_ok=True)
+    deps = _headers()
+    objs = []
+    for s in SOURCES:
+        src = os.path.join(CSRC, s)
+        obj = os.path.join(BUILD, s + ".o")
+        objs.append(obj)
+        if _newer(src, obj, deps):
+            cmd = [NVCC] + _flags() + ["-c", src, "-o", obj]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+    if any(_newer(o, LIB, []) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-Xcompiler", "-fopenmp", "-ldl", "-lgomp"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv)
+    print(LIB)

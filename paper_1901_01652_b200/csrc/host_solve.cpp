@@ -1,0 +1,664 @@
+// SPDX-License-Identifier: Apache-2.0
+// Host small solve on P: trals / trsvd (see host_solve.hpp for the contract).
+#include "host_solve.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+#include "random_host.hpp"
+
+namespace trg {
+namespace host {
+
+namespace {
+
+void require(bool ok, const std::string& msg) {
+    if (!ok) throw std::invalid_argument(msg);
+}
+
+idx prod(const std::vector<idx>& v) {
+    idx p = 1;
+    for (idx d : v) p *= d;
+    return p;
+}
+
+Tensor make(std::vector<idx> shape) {
+    Tensor t;
+    t.shape = std::move(shape);
+    t.data.assign(static_cast<size_t>(prod(t.shape)), 0.0);
+    return t;
+}
+
+struct Split {
+    idx left, dim, right;
+};
+Split split(const std::vector<idx>& s, idx mode) {
+    Split r{1, s[static_cast<size_t>(mode)], 1};
+    for (idx n = 0; n < mode; ++n) r.left *= s[static_cast<size_t>(n)];
+    for (idx n = mode + 1; n < static_cast<idx>(s.size()); ++n) r.right *= s[static_cast<size_t>(n)];
+    return r;
+}
+
+// unfold_tr (tensor.hpp:147-157): m(d, r + right*l) = t[l + left*(d + dim*r)]
+Mat unfold_tr(const Tensor& t, idx mode) {
+    const Split s = split(t.shape, mode);
+    Mat m(s.dim, s.left * s.right);
+    for (idx l = 0; l < s.left; ++l)
+        for (idx r = 0; r < s.right; ++r)
+            for (idx d = 0; d < s.dim; ++d) m(d, r + s.right * l) = t.data[static_cast<size_t>(l + s.left * (d + s.dim * r))];
+    return m;
+}
+
+// unfold_classic at mode 1 of a core (R_n, I_n, R_{n+1}) -> I_n x (R_n R_{n+1})
+Mat core_unfold1(const Tensor& g) {
+    const idx ra = g.shape[0], i = g.shape[1], rb = g.shape[2];
+    Mat m(i, ra * rb);
+    for (idx b = 0; b < rb; ++b)
+        for (idx d = 0; d < i; ++d)
+            for (idx a = 0; a < ra; ++a) m(d, a + ra * b) = g.data[static_cast<size_t>(a + ra * (d + i * b))];
+    return m;
+}
+
+Mat transpose(const Mat& m) {
+    Mat t(m.c, m.r);
+    for (idx j = 0; j < m.c; ++j)
+        for (idx i = 0; i < m.r; ++i) t(j, i) = m(i, j);
+    return t;
+}
+
+Mat matmul(const Mat& A, const Mat& B) {
+    Mat C(A.r, B.c);
+#pragma omp parallel for schedule(static) if (A.r * B.c * A.c > (1 << 18))
+    for (idx j = 0; j < B.c; ++j) {
+        double* cj = C.col(j);
+        for (idx k = 0; k < A.c; ++k) {
+            const double b = B(k, j);
+            const double* ak = A.col(k);
+            for (idx i = 0; i < A.r; ++i) cj[i] += ak[i] * b;
+        }
+    }
+    return C;
+}
+
+Mat matmul_tn(const Mat& A, const Mat& B) {
+    Mat C(A.c, B.c);
+#pragma omp parallel for schedule(static) if (A.r * B.c * A.c > (1 << 18))
+    for (idx j = 0; j < B.c; ++j)
+        for (idx i = 0; i < A.c; ++i) {
+            const double* ai = A.col(i);
+            const double* bj = B.col(j);
+            double s = 0.0;
+            for (idx k = 0; k < A.r; ++k) s += ai[k] * bj[k];
+            C(i, j) = s;
+        }
+    return C;
+}
+
+// chain_contract (tr_factors.hpp:92-102)
+Tensor chain(const Tensor& a, const Tensor& g) {
+    const idx ra = a.shape[0], p = a.shape[1], rb = a.shape[2];
+    const idx i = g.shape[1], rc = g.shape[2];
+    Tensor out = make({ra, p * i, rc});
+    const idx M = ra * p, Nc = i * rc;
+#pragma omp parallel for schedule(static) if (M * Nc * rb > (1 << 18))
+    for (idx j = 0; j < Nc; ++j) {
+        double* oj = out.data.data() + M * j;
+        for (idx k = 0; k < rb; ++k) {
+            const double w = g.data[static_cast<size_t>(k + rb * j)];
+            const double* ak = a.data.data() + M * k;
+            for (idx r = 0; r < M; ++r) oj[r] += ak[r] * w;
+        }
+    }
+    return out;
+}
+
+// subchain (tr_factors.hpp:111-119)
+Tensor subchain(const Cores& f, idx mode) {
+    const idx N = f.order();
+    Tensor cur = f.g[static_cast<size_t>((mode + 1) % N)];
+    for (idx s = 2; s < N; ++s) cur = chain(cur, f.g[static_cast<size_t>((mode + s) % N)]);
+    return cur;
+}
+
+// ---------------------------------------------------------------- QR / LS
+struct HQR {
+    Mat qr;
+    std::vector<double> tau;
+    explicit HQR(const Mat& a) : qr(a) {
+        const idx m = qr.r, n = qr.c, k = std::min(m, n);
+        tau.assign(static_cast<size_t>(k), 0.0);
+        for (idx j = 0; j < k; ++j) {
+            double* cj = qr.col(j);
+            const double c0 = cj[j];
+            double tail = 0.0;
+            for (idx i = j + 1; i < m; ++i) tail += cj[i] * cj[i];
+            double beta, t;
+            if (tail <= std::numeric_limits<double>::min()) {  // Eigen makeHouseholder
+                t = 0.0;
+                beta = c0;
+                for (idx i = j + 1; i < m; ++i) cj[i] = 0.0;
+            } else {
+                beta = std::sqrt(c0 * c0 + tail);
+                if (c0 >= 0.0) beta = -beta;
+                const double inv = 1.0 / (c0 - beta);
+                for (idx i = j + 1; i < m; ++i) cj[i] *= inv;
+                t = (beta - c0) / beta;
+            }
+            cj[j] = beta;
+            tau[static_cast<size_t>(j)] = t;
+            if (t == 0.0) continue;
+#pragma omp parallel for schedule(static) if ((n - j) * (m - j) > (1 << 15))
+            for (idx c = j + 1; c < n; ++c) {
+                double* cc = qr.col(c);
+                double w = cc[j];
+                for (idx i = j + 1; i < m; ++i) w += cj[i] * cc[i];
+                w *= t;
+                cc[j] -= w;
+                for (idx i = j + 1; i < m; ++i) cc[i] -= w * cj[i];
+            }
+        }
+    }
+    Mat solve(const Mat& b) const {
+        const idx m = qr.r, n = qr.c, k = static_cast<idx>(tau.size());
+        Mat y = b;
+        for (idx j = 0; j < k; ++j) {
+            const double t = tau[static_cast<size_t>(j)];
+            if (t == 0.0) continue;
+            const double* v = qr.col(j);
+#pragma omp parallel for schedule(static) if (y.c * (m - j) > (1 << 15))
+            for (idx c = 0; c < y.c; ++c) {
+                double* bc = y.col(c);
+                double w = bc[j];
+                for (idx i = j + 1; i < m; ++i) w += v[i] * bc[i];
+                w *= t;
+                bc[j] -= w;
+                for (idx i = j + 1; i < m; ++i) bc[i] -= w * v[i];
+            }
+        }
+        Mat x(n, b.c);
+#pragma omp parallel for schedule(static) if (b.c * n * n > (1 << 16))
+        for (idx c = 0; c < b.c; ++c)
+            for (idx i = n - 1; i >= 0; --i) {
+                double s = y(i, c);
+                for (idx j = i + 1; j < n; ++j) s -= qr(i, j) * x(j, c);
+                x(i, c) = s / qr(i, i);
+            }
+        return x;
+    }
+};
+
+bool cholesky(const Mat& a, Mat& L) {
+    const idx n = a.r;
+    L = Mat(n, n);
+    for (idx j = 0; j < n; ++j) {
+        double d = a(j, j);
+        for (idx k = 0; k < j; ++k) d -= L(j, k) * L(j, k);
+        if (!(d > 0.0)) return false;
+        const double l = std::sqrt(d);
+        L(j, j) = l;
+        for (idx i = j + 1; i < n; ++i) {
+            double s = a(i, j);
+            for (idx k = 0; k < j; ++k) s -= L(i, k) * L(j, k);
+            L(i, j) = s / l;
+        }
+    }
+    return true;
+}
+
+Mat chol_solve(const Mat& L, const Mat& b) {
+    const idx n = L.r;
+    Mat x = b;
+#pragma omp parallel for schedule(static) if (b.c * n * n > (1 << 16))
+    for (idx c = 0; c < b.c; ++c) {
+        double* xc = x.col(c);
+        for (idx i = 0; i < n; ++i) {
+            double s = xc[i];
+            for (idx k = 0; k < i; ++k) s -= L(i, k) * xc[k];
+            xc[i] = s / L(i, i);
+        }
+        for (idx i = n - 1; i >= 0; --i) {
+            double s = xc[i];
+            for (idx k = i + 1; k < n; ++k) s -= L(k, i) * xc[k];
+            xc[i] = s / L(i, i);
+        }
+    }
+    return x;
+}
+
+// LDL^T with symmetric pivoting (Eigen::LDLT semantics), used by ridge_solve.
+Mat ldlt_solve(Mat a, const Mat& b) {
+    const idx n = a.r;
+    std::vector<idx> perm(static_cast<size_t>(n));
+    std::iota(perm.begin(), perm.end(), 0);
+    for (idx k = 0; k < n; ++k) {
+        idx p = k;
+        double best = std::abs(a(k, k));
+        for (idx i = k + 1; i < n; ++i)
+            if (std::abs(a(i, i)) > best) {
+                best = std::abs(a(i, i));
+                p = i;
+            }
+        if (p != k) {
+            std::swap(perm[static_cast<size_t>(k)], perm[static_cast<size_t>(p)]);
+            for (idx j = 0; j < n; ++j) std::swap(a(k, j), a(p, j));
+            for (idx i = 0; i < n; ++i) std::swap(a(i, k), a(i, p));
+        }
+        const double d = a(k, k);
+        if (d == 0.0) continue;
+        for (idx i = k + 1; i < n; ++i) {
+            const double lik = a(i, k) / d;
+            for (idx j = k + 1; j <= i; ++j) a(i, j) -= lik * a(j, k);
+        }
+        for (idx i = k + 1; i < n; ++i) a(i, k) /= d;
+        for (idx i = k + 1; i < n; ++i) a(k, i) = a(i, k);
+        for (idx i = k + 1; i < n; ++i)
+            for (idx j = k + 1; j < i; ++j) a(j, i) = a(i, j);
+    }
+    Mat x(n, b.c);
+    std::vector<double> y(static_cast<size_t>(n));
+    for (idx c = 0; c < b.c; ++c) {
+        for (idx i = 0; i < n; ++i) y[static_cast<size_t>(i)] = b(perm[static_cast<size_t>(i)], c);
+        for (idx i = 0; i < n; ++i)
+            for (idx k = 0; k < i; ++k) y[static_cast<size_t>(i)] -= a(i, k) * y[static_cast<size_t>(k)];
+        for (idx i = 0; i < n; ++i) y[static_cast<size_t>(i)] = a(i, i) != 0.0 ? y[static_cast<size_t>(i)] / a(i, i) : 0.0;
+        for (idx i = n - 1; i >= 0; --i)
+            for (idx k = i + 1; k < n; ++k) y[static_cast<size_t>(i)] -= a(k, i) * y[static_cast<size_t>(k)];
+        for (idx i = 0; i < n; ++i) x(perm[static_cast<size_t>(i)], c) = y[static_cast<size_t>(i)];
+    }
+    return x;
+}
+
+// solvers.hpp:186-190
+Mat ridge_solve(Mat gram, const Mat& rhs) {
+    double tr = 0.0;
+    for (idx i = 0; i < gram.r; ++i) tr += gram(i, i);
+    const double lambda = 1e-12 * tr / static_cast<double>(gram.r);
+    for (idx i = 0; i < gram.r; ++i) gram(i, i) += lambda;
+    return ldlt_solve(std::move(gram), rhs);
+}
+
+// solvers.hpp:195-205
+Mat ls_solve_qr(const Mat& a, const Mat& b) {
+    if (a.r >= a.c) {
+        HQR qr(a);
+        double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
+        for (idx i = 0; i < a.c; ++i) {
+            dmax = std::max(dmax, std::abs(qr.qr(i, i)));
+            dmin = std::min(dmin, std::abs(qr.qr(i, i)));
+        }
+        const double cutoff = dmax * static_cast<double>(std::max(a.r, a.c)) * std::numeric_limits<double>::epsilon() * 16.0;
+        if (dmax > 0.0 && dmin > cutoff) return qr.solve(b);
+    }
+    return ridge_solve(matmul_tn(a, a), matmul_tn(a, b));
+}
+
+// solvers.hpp:209-219
+Mat ls_solve_gram(const Mat& gram, const Mat& rhs) {
+    Mat L;
+    if (cholesky(gram, L)) {
+        double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
+        for (idx i = 0; i < L.r; ++i) {
+            dmax = std::max(dmax, std::abs(L(i, i)));
+            dmin = std::min(dmin, std::abs(L(i, i)));
+        }
+        const double cutoff = dmax * static_cast<double>(gram.r) * std::numeric_limits<double>::epsilon() * 16.0;
+        if (dmax > 0.0 && dmin > cutoff) return chol_solve(L, rhs);
+    }
+    return ridge_solve(gram, rhs);
+}
+
+// solvers.hpp:102-129: Gram of the subchain's mode-2 TR unfolding via per-core transfer matrices
+Mat subchain_gram(const Cores& f, idx n) {
+    const idx N = f.order();
+    Mat omega;
+    for (idx s = 1; s < N; ++s) {
+        const Tensor& g = f.g[static_cast<size_t>((n + s) % N)];
+        const idx rk = g.shape[0], rk1 = g.shape[2];
+        const Mat h = core_unfold1(g);
+        const Mat gram = matmul_tn(h, h);
+        Mat w(rk * rk, rk1 * rk1);
+        for (idx s2 = 0; s2 < rk1; ++s2)
+            for (idx s1 = 0; s1 < rk1; ++s1)
+                for (idx r2 = 0; r2 < rk; ++r2)
+                    for (idx r1 = 0; r1 < rk; ++r1) w(r1 + rk * r2, s1 + rk1 * s2) = gram(r1 + rk * s1, r2 + rk * s2);
+        omega = (s == 1) ? std::move(w) : matmul(omega, w);
+    }
+    const idx rn = f.rank(n), rn1 = f.rank((n + 1) % N);
+    Mat m(rn * rn1, rn * rn1);
+    for (idx b2 = 0; b2 < rn1; ++b2)
+        for (idx a2 = 0; a2 < rn; ++a2)
+            for (idx b = 0; b < rn1; ++b)
+                for (idx a = 0; a < rn; ++a) m(a + rn * b, a2 + rn * b2) = omega(b + rn1 * b2, a + rn * a2);
+    return m;
+}
+
+// solvers.hpp:134-182: V = X_<n> S one core at a time
+Mat subchain_rhs(const Mat& xn_tr, const Cores& f, idx n) {
+    const idx N = f.order();
+    const idx dim_n = xn_tr.r;
+    const Mat b = transpose(xn_tr);
+    const Tensor& g0 = f.g[static_cast<size_t>((n + 1) % N)];
+    const idx r0 = g0.shape[0], i0 = g0.shape[1], s0 = g0.shape[2];
+    Mat ghat(r0 * s0, i0);
+    for (idx i = 0; i < i0; ++i)
+        for (idx s = 0; s < s0; ++s)
+            for (idx r = 0; r < r0; ++r) ghat(r + r0 * s, i) = g0.data[static_cast<size_t>(r + r0 * (i + i0 * s))];
+    Mat bm(i0, static_cast<idx>(b.a.size()) / i0);
+    bm.a = b.a;
+    Mat cur = matmul(ghat, bm);
+    const idx front = r0;
+    for (idx s = 2; s < N; ++s) {
+        const Tensor& g = f.g[static_cast<size_t>((n + s) % N)];
+        const idx rk = g.shape[0], ik = g.shape[1], rk1 = g.shape[2];
+        const idx mid = rk * ik;
+        const idx tail = static_cast<idx>(cur.a.size()) / (front * mid);
+        Mat next(front * rk1, tail);
+#pragma omp parallel for schedule(static) if (tail * front * mid * rk1 > (1 << 18))
+        for (idx t = 0; t < tail; ++t) {
+            const double* in = cur.a.data() + front * mid * t;
+            double* out = next.a.data() + front * rk1 * t;
+            for (idx c = 0; c < rk1; ++c)
+                for (idx q = 0; q < mid; ++q) {
+                    const double w = g.data[static_cast<size_t>(q + mid * c)];
+                    for (idx r = 0; r < front; ++r) out[r + front * c] += in[r + front * q] * w;
+                }
+        }
+        cur = std::move(next);
+    }
+    const idx rn = f.rank(n), rn1 = front;
+    Mat v(dim_n, rn * rn1);
+    for (idx i = 0; i < dim_n; ++i)
+        for (idx a = 0; a < rn; ++a)
+            for (idx bb = 0; bb < rn1; ++bb) v(i, a + rn * bb) = cur.a[static_cast<size_t>(bb + rn1 * (a + rn * i))];
+    return v;
+}
+
+// solvers.hpp:223-230
+void store_core(Tensor& core, const Mat& z) {
+    const idx rn = core.shape[0], in = core.shape[1], rn1 = core.shape[2];
+    for (idx s = 0; s < rn1; ++s)
+        for (idx i = 0; i < in; ++i)
+            for (idx r = 0; r < rn; ++r) core.data[static_cast<size_t>(r + rn * (i + in * s))] = z(r + rn * s, i);
+}
+
+constexpr idx kDirectLsMaxRows = 4096;  // solvers.hpp:234
+
+// solvers.hpp:238-251
+void als_update_mode(const Mat& xn_tr, Cores& f, idx n) {
+    const idx n_cols = xn_tr.c;
+    const idx m = f.rank(n) * f.rank((n + 1) % f.order());
+    Mat z;
+    if (n_cols <= kDirectLsMaxRows && n_cols >= m) {
+        const Tensor s = subchain(f, n);
+        z = ls_solve_qr(unfold_tr(s, 1), transpose(xn_tr));
+    } else {
+        z = ls_solve_gram(subchain_gram(f, n), transpose(subchain_rhs(xn_tr, f, n)));
+    }
+    store_core(f.g[static_cast<size_t>(n)], z);
+}
+
+double fnorm(const Tensor& t) {
+    double s = 0.0;
+    for (double v : t.data) s += v * v;
+    return std::sqrt(s);
+}
+
+SolveOut order_one(const Tensor& x, idx r0) {  // solvers.hpp:268-279
+    Tensor core = make({r0, x.shape[0], r0});
+    for (idx i = 0; i < x.shape[0]; ++i) core.data[static_cast<size_t>(r0 * i)] = x.data[static_cast<size_t>(i)];
+    SolveOut o;
+    o.cores.g.push_back(std::move(core));
+    o.rse_history = {fnorm(x) > 0.0 ? rse(x, reconstruct_full(o.cores)) : 0.0};
+    o.sweeps_run = 1;
+    return o;
+}
+
+SolveOut zero_report(const Tensor& x, const std::vector<idx>& ranks) {  // solvers.hpp:281-290
+    SolveOut o;
+    const idx N = x.order();
+    for (idx n = 0; n < N; ++n)
+        o.cores.g.push_back(make({ranks[static_cast<size_t>(n)], x.shape[static_cast<size_t>(n)],
+                                  ranks[static_cast<size_t>((n + 1) % N)]}));
+    o.rse_history = {0.0};
+    return o;
+}
+
+// one-sided Jacobi thin SVD, singular values descending (BDCSVD stand-in)
+void svd(const Mat& a, Mat& U, std::vector<double>& s, Mat& V) {
+    const bool wide = a.r < a.c;
+    Mat W = wide ? transpose(a) : a;
+    const idx m = W.r, n = W.c;
+    Mat Vw(n, n);
+    for (idx i = 0; i < n; ++i) Vw(i, i) = 1.0;
+    for (int sweep = 0; sweep < 80; ++sweep) {
+        bool rotated = false;
+        for (idx p = 0; p < n - 1; ++p)
+            for (idx q = p + 1; q < n; ++q) {
+                double* wp = W.col(p);
+                double* wq = W.col(q);
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (idx i = 0; i < m; ++i) {
+                    al += wp[i] * wp[i];
+                    be += wq[i] * wq[i];
+                    ga += wp[i] * wq[i];
+                }
+                if (ga == 0.0 || std::abs(ga) <= 1e-15 * std::sqrt(al * be)) continue;
+                rotated = true;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+                for (idx i = 0; i < m; ++i) {
+                    const double x = wp[i], y = wq[i];
+                    wp[i] = c * x - sn * y;
+                    wq[i] = sn * x + c * y;
+                }
+                double* vp = Vw.col(p);
+                double* vq = Vw.col(q);
+                for (idx i = 0; i < n; ++i) {
+                    const double x = vp[i], y = vq[i];
+                    vp[i] = c * x - sn * y;
+                    vq[i] = sn * x + c * y;
+                }
+            }
+        if (!rotated) break;
+    }
+    std::vector<double> sv(static_cast<size_t>(n));
+    for (idx j = 0; j < n; ++j) {
+        double q = 0.0;
+        for (idx i = 0; i < m; ++i) q += W(i, j) * W(i, j);
+        sv[static_cast<size_t>(j)] = std::sqrt(q);
+    }
+    std::vector<idx> ord(static_cast<size_t>(n));
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](idx x, idx y) { return sv[static_cast<size_t>(x)] > sv[static_cast<size_t>(y)]; });
+    Mat Us(m, n), Vs(n, n);
+    s.assign(static_cast<size_t>(n), 0.0);
+    for (idx j = 0; j < n; ++j) {
+        const idx src = ord[static_cast<size_t>(j)];
+        const double sj = sv[static_cast<size_t>(src)];
+        s[static_cast<size_t>(j)] = sj;
+        for (idx i = 0; i < m; ++i) Us(i, j) = sj > 0.0 ? W(i, src) / sj : 0.0;
+        for (idx i = 0; i < n; ++i) Vs(i, j) = Vw(i, src);
+    }
+    if (wide) {
+        U = std::move(Vs);
+        V = std::move(Us);
+    } else {
+        U = std::move(Us);
+        V = std::move(Vs);
+    }
+}
+
+idx truncation_rank(const std::vector<double>& sv, double budget_sq, double* disc) {  // solvers.hpp:347-358
+    idx r = static_cast<idx>(sv.size());
+    double tail = 0.0;
+    while (r > 1) {
+        const double t = tail + sv[static_cast<size_t>(r - 1)] * sv[static_cast<size_t>(r - 1)];
+        if (t > budget_sq) break;
+        tail = t;
+        --r;
+    }
+    *disc += tail;
+    return r;
+}
+
+std::pair<idx, idx> balanced_divisor_split(idx r) {  // solvers.hpp:361-371
+    idx target = static_cast<idx>(std::sqrt(static_cast<double>(r)));
+    while ((target + 1) * (target + 1) <= r) ++target;
+    while (target > 1 && target * target > r) --target;
+    idx best = 1;
+    for (idx d = 1; d <= r; ++d) {
+        if (r % d != 0) continue;
+        if (std::abs(d - target) < std::abs(best - target)) best = d;
+    }
+    return {best, r / best};
+}
+
+}  // namespace
+
+// tr_factors.hpp:123-137 at mode 0: X_<0> = G_{0,(2)} S^T, folded (mode 0 fold is free)
+Tensor reconstruct_full(const Cores& f) {
+    const idx N = f.order();
+    std::vector<idx> shape;
+    for (idx n = 0; n < N; ++n) shape.push_back(f.dim(n));
+    Tensor out = make(shape);
+    if (N == 1) {
+        const Tensor& g = f.g[0];
+        const idx r = g.shape[0], I = g.shape[1];
+        for (idx i = 0; i < I; ++i) {
+            double tr = 0.0;
+            for (idx a = 0; a < std::min(r, g.shape[2]); ++a) tr += g.data[static_cast<size_t>(a + r * (i + I * a))];
+            out.data[static_cast<size_t>(i)] = tr;
+        }
+        return out;
+    }
+    const Mat core2 = core_unfold1(f.g[0]);      // I_0 x (R_0 R_1)
+    const Tensor s = subchain(f, 0);             // (R_1, P, R_0)
+    const idx R1 = s.shape[0], P = s.shape[1], R0 = s.shape[2], I0 = core2.r;
+#pragma omp parallel for schedule(static) if (I0 * P * R0 * R1 > (1 << 18))
+    for (idx p = 0; p < P; ++p) {
+        double* xp = out.data.data() + I0 * p;
+        for (idx b = 0; b < R1; ++b)
+            for (idx a = 0; a < R0; ++a) {
+                const double w = s.data[static_cast<size_t>(b + R1 * (p + P * a))];
+                const double* ck = core2.col(a + R0 * b);
+                for (idx i = 0; i < I0; ++i) xp[i] += ck[i] * w;
+            }
+    }
+    return out;
+}
+
+double rse(const Tensor& ref, const Tensor& approx) {  // solvers.hpp:47-54
+    require(ref.shape == approx.shape, "rse: shape mismatch");
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < ref.data.size(); ++i) {
+        const double d = ref.data[i] - approx.data[i];
+        num += d * d;
+        den += ref.data[i] * ref.data[i];
+    }
+    require(den > 0.0, "rse: reference tensor has zero norm");
+    return std::sqrt(num) / std::sqrt(den);
+}
+
+SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance, idx max_sweeps, std::uint64_t seed) {
+    require(static_cast<idx>(ranks.size()) == x.order(), "trals: rank vector length must equal tensor order");
+    for (idx r : ranks) require(r >= 1, "trals: ranks must be positive");
+    require(max_sweeps >= 1, "trals: max_sweeps must be positive");
+    const double xnorm = fnorm(x);
+    if (xnorm == 0.0) return zero_report(x, ranks);
+    if (x.order() == 1) return order_one(x, ranks[0]);
+    const idx N = x.order();
+    // init_factors (solvers.hpp:80-95)
+    Cores f;
+    double pr = 1.0;
+    for (idx r : ranks) pr *= static_cast<double>(r);
+    const double scale = std::pow(xnorm / pr, 1.0 / static_cast<double>(N));
+    GaussianStream gs(seed);
+    for (idx n = 0; n < N; ++n) {
+        Tensor core = make({ranks[static_cast<size_t>(n)], x.shape[static_cast<size_t>(n)], ranks[static_cast<size_t>((n + 1) % N)]});
+        for (auto& v : core.data) v = scale * gs.next();
+        f.g.push_back(std::move(core));
+    }
+    std::vector<Mat> unf;
+    for (idx n = 0; n < N; ++n) unf.push_back(unfold_tr(x, n));
+    SolveOut o;
+    for (idx sweep = 1; sweep <= max_sweeps; ++sweep) {
+        for (idx n = 0; n < N; ++n) als_update_mode(unf[static_cast<size_t>(n)], f, n);
+        o.rse_history.push_back(rse(x, reconstruct_full(f)));
+        o.sweeps_run = sweep;
+        const size_t k = o.rse_history.size();
+        if (k >= 2 && std::abs(o.rse_history[k - 1] - o.rse_history[k - 2]) < tolerance * o.rse_history[k - 2]) break;
+    }
+    o.cores = std::move(f);
+    return o;
+}
+
+SolveOut trsvd(const Tensor& x, double tolerance) {
+    require(tolerance >= 0.0, "trsvd: tolerance must be nonnegative");
+    const idx order = x.order();
+    const double xnorm = fnorm(x);
+    if (order == 1) return order_one(x, 1);
+    if (xnorm == 0.0) return zero_report(x, std::vector<idx>(static_cast<size_t>(order), 1));
+    const double budget = tolerance * xnorm / std::sqrt(static_cast<double>(order));
+    const double budget_sq = budget * budget;
+    double disc = 0.0;
+    const idx dim0 = x.shape[0];
+    const idx rest = x.size() / dim0;
+    Mat m0(dim0, rest);
+    m0.a = x.data;
+    Mat U, V;
+    std::vector<double> s;
+    svd(m0, U, s, V);
+    const idx r01 = truncation_rank(s, budget_sq, &disc);
+    const auto [ra, rb] = balanced_divisor_split(r01);
+    SolveOut o;
+    o.cores.g.resize(static_cast<size_t>(order));
+    {
+        Tensor g0 = make({ra, dim0, rb});
+        for (idx q = 0; q < rb; ++q)
+            for (idx i = 0; i < dim0; ++i)
+                for (idx p = 0; p < ra; ++p) g0.data[static_cast<size_t>(p + ra * (i + dim0 * q))] = U(i, p + ra * q);
+        o.cores.g[0] = std::move(g0);
+    }
+    std::vector<double> cur(static_cast<size_t>(r01 * rest));
+    for (idx p = 0; p < ra; ++p)
+        for (idx c = 0; c < rest; ++c)
+            for (idx q = 0; q < rb; ++q) {
+                const idx row = p + ra * q;
+                cur[static_cast<size_t>(q + rb * c + rb * rest * p)] = s[static_cast<size_t>(row)] * V(c, row);
+            }
+    idx lead = rb;
+    for (idx k = 1; k + 1 < order; ++k) {
+        const idx dk = x.shape[static_cast<size_t>(k)];
+        const idx rows = lead * dk;
+        const idx cols = static_cast<idx>(cur.size()) / rows;
+        Mat mk(rows, cols);
+        mk.a = cur;
+        svd(mk, U, s, V);
+        const idx r = truncation_rank(s, budget_sq, &disc);
+        Tensor gk = make({lead, dk, r});
+        for (idx j = 0; j < r; ++j)
+            for (idx i = 0; i < rows; ++i) gk.data[static_cast<size_t>(i + rows * j)] = U(i, j);
+        o.cores.g[static_cast<size_t>(k)] = std::move(gk);
+        std::vector<double> next(static_cast<size_t>(r * cols));
+        for (idx c = 0; c < cols; ++c)
+            for (idx j = 0; j < r; ++j) next[static_cast<size_t>(j + r * c)] = s[static_cast<size_t>(j)] * V(c, j);
+        cur = std::move(next);
+        lead = r;
+    }
+    {
+        Tensor gl;
+        gl.shape = {lead, x.shape[static_cast<size_t>(order - 1)], ra};
+        gl.data = std::move(cur);
+        o.cores.g[static_cast<size_t>(order - 1)] = std::move(gl);
+    }
+    o.rse_history = {rse(x, reconstruct_full(o.cores))};
+    o.sweeps_run = 1;
+    o.discarded_sq = disc;
+    return o;
+}
+
+}  // namespace host
+}  // namespace trg

@@ -1,0 +1,67 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host-side small TR solve on the projected tensor P (Alg. 1 line 9).
+//
+// P is tiny (prod K_n <= ~10^6 entries), so trals / trsvd run on the host in
+// fp64 exactly as the reference specifies them; only the streaming passes
+// over X are device work. This is product code: it is
+// the drop-in for solvers.hpp:297-459 with the same results up to rounding:
+//   trals  solvers.hpp:297-334 (init_factors :80-95, als_update_mode :238-251,
+//          direct QR route :195-205 / Gram route :102-219, kDirectLsMaxRows 4096)
+//   trsvd  solvers.hpp:382-459 (truncation_rank :347-358,
+//          balanced_divisor_split :361-371)
+// Eigen's BDCSVD is replaced by one-sided Jacobi (singular vectors equal up to
+// sign). Loops that write disjoint outputs are OpenMP-parallel, which keeps
+// results bit-identical for any thread count.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace trg {
+namespace host {
+
+using idx = std::int64_t;
+
+struct Mat {
+    idx r = 0, c = 0;
+    std::vector<double> a;
+    Mat() = default;
+    Mat(idx rows, idx cols) : r(rows), c(cols), a(static_cast<size_t>(rows * cols), 0.0) {}
+    double& operator()(idx i, idx j) { return a[static_cast<size_t>(i + r * j)]; }
+    double operator()(idx i, idx j) const { return a[static_cast<size_t>(i + r * j)]; }
+    double* col(idx j) { return a.data() + r * j; }
+    const double* col(idx j) const { return a.data() + r * j; }
+};
+
+// Dense tensor, first-index-fastest (tensor.hpp:33-38).
+struct Tensor {
+    std::vector<idx> shape;
+    std::vector<double> data;
+    idx size() const { return static_cast<idx>(data.size()); }
+    idx order() const { return static_cast<idx>(shape.size()); }
+};
+
+struct Cores {
+    std::vector<Tensor> g;  // core n: (R_n, I_n, R_{n+1})
+    idx order() const { return static_cast<idx>(g.size()); }
+    idx rank(idx n) const { return g[static_cast<size_t>(n)].shape[0]; }
+    idx dim(idx n) const { return g[static_cast<size_t>(n)].shape[1]; }
+};
+
+struct SolveOut {
+    Cores cores;
+    std::vector<double> rse_history;
+    idx sweeps_run = 0;
+    double discarded_sq = 0.0;
+};
+
+SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance, idx max_sweeps, std::uint64_t seed);
+SolveOut trsvd(const Tensor& x, double tolerance);
+Tensor reconstruct_full(const Cores& f);
+double rse(const Tensor& ref, const Tensor& approx);
+
+}  // namespace host
+}  // namespace trg

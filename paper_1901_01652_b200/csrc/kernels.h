@@ -1,0 +1,87 @@
+// SPDX-License-Identifier: Apache-2.0
+// Host-side launchers for the libtrg sm_100a kernels. Internal to libtrg.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace trg {
+
+enum DType { F32 = 0, F64 = 1 };
+
+inline size_t dtype_size(int dt) { return dt == F64 ? 8 : 4; }
+
+// ---- sketch: Y_n = P_(n) * Omega_n (K1), deterministic split-K -------------
+// The current tensor is read as (left, dim, right) (tensor.hpp:112-123);
+// unfold_classic column c = l + left*r (tensor.hpp:133-142). Omega_n(c, k) is
+// reference draw D + col_off + c + rows_glob*k of the single stream `seed`
+// (sketch.hpp:32-38, 69, 81). Result Y is dim x K column-major fp64.
+struct SketchPlan {
+    int dtype;
+    int64_t left, dim, right;  // local view
+    int K;
+    uint64_t seed, D;
+    int64_t rows_glob, col_off;
+    // derived by plan_sketch()
+    int TD, TK, Kp, DT, CT, nd, nk, G, threads, ndt;
+    int64_t ncols, ntiles;
+    int grid_x;
+    size_t smem;
+    size_t partial_elems;  // grid_x * dim * K doubles
+};
+void plan_sketch(SketchPlan& p, int num_sms);
+void launch_sketch(const SketchPlan& p, const void* x, double* partial, double* y, cudaStream_t s);
+
+// ---- mode-n product out = in x_n M (K2 shrink with M = Q^T, K7 lift with M = Q)
+// M(o, d) = m[o*m_so + d*m_sd] (fp64). out has odim in place of dim.
+struct TTMPlan {
+    int dtype;
+    int64_t left, dim, right, odim;
+    int64_t m_so, m_sd;
+    // derived
+    int TM, TO, MT, DT, nm, no, OT, threads, noT;
+    int64_t rows, nrowtiles;
+    int grid_x;
+    size_t smem;
+};
+void plan_ttm(TTMPlan& p, int num_sms);
+void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cudaStream_t s);
+
+// ---- thin QR with diag(R) >= 0 (K4): CholQR2 + Householder fallback, fp64.
+// Y is m x k column-major; Q (m x k) out. work >= m*k doubles + 2*k.
+void launch_qr(const double* y, int64_t m, int k, double* q, double* work, int* flag, cudaStream_t s);
+
+// ---- Gaussian test-matrix export (parity): out(c, k) = draw off + c + rows*k
+void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, double* out, cudaStream_t s);
+
+// ---- TR model on device ------------------------------------------------------
+// chain_contract (tr_factors.hpp:92-102): (Ra,P,Rb) o (Rb,I,Rc) -> (Ra,P*I,Rc), fp64
+void launch_chain(const double* a, int64_t ra, int64_t p, int64_t rb, const double* g, int64_t i, int64_t rc,
+                  double* out, cudaStream_t s);
+// X(i0, p) = sum_{a,b} G0(a, i0, b) S(b, p, a) over the local columns p:
+// mode 0 writes X (dtype) ; mode 1 accumulates per-block (sum (x - xhat)^2, sum x^2).
+struct ReconPlan {
+    int dtype;
+    int64_t I0, P, R0, R1;
+    int grid_x, grid_y, threads;
+    size_t smem;
+    int nblocks;
+};
+void plan_recon(ReconPlan& p, int num_sms);
+void launch_recon(const ReconPlan& p, const double* g0, const double* S, void* x, int write_mode, double* block_sums,
+                  cudaStream_t s);
+// sum of block partial pairs in fixed order -> out[0..1]
+void launch_sum_pairs(const double* block_sums, int nblocks, double* out, cudaStream_t s);
+// noise: sums of x^2 and e^2 (e = draws off..off+n-1), then x += alpha*e
+void launch_noise_norms(const void* x, int dtype, int64_t n, uint64_t seed, uint64_t off, double* block_sums,
+                        int nblocks, cudaStream_t s);
+void launch_add_noise(void* x, int dtype, int64_t n, uint64_t seed, uint64_t off, double alpha, cudaStream_t s);
+// y = alpha * x + beta (affine rescale, used by the hyperspectral synthesizer)
+void launch_minmax(const void* x, int dtype, int64_t n, double* block_mm, int nblocks, cudaStream_t s);
+void launch_affine(void* x, int dtype, int64_t n, double a, double b, cudaStream_t s);
+// dtype conversion helpers
+void launch_convert(const void* in, int in_dt, void* out, int out_dt, int64_t n, cudaStream_t s);
+// scatter rows [lo, lo+rows) of a (rows x k) column-major matrix into a zeroed (m x k) matrix
+void launch_scatter_rows(const double* in, int64_t rows, int k, int64_t lo, int64_t m, double* out, cudaStream_t s);
+
+}  // namespace trg

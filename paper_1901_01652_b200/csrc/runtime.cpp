@@ -1,0 +1,1078 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// libtrg host runtime: contexts, device tensors, the per-mode projection
+// pipeline, back-projection, RSE and Algorithm 1 orchestration behind the
+// C ABI of include/trg.h.
+//
+// Reference map:
+//   trg_sketch_run      sketch                 sketch.hpp:62-89
+//   trg_back_project    back_project           sketch.hpp:106-122
+//   trg_rse             rse(x, reconstruct_full) solvers.hpp:47-54, tr_factors.hpp:123-137
+//   trg_decompose       randomized_decompose    sketch.hpp:126-147 (rtrals :154, rtrsvd :161)
+//   trg_omega           gaussian_matrix         sketch.hpp:32-38
+//   trg_mode_n_product  mode_n_product          tensor.hpp:193-207
+//
+// Everything between the first sketch kernel and "P and all Q_n resident" is
+// stream-ordered device work with no host round trip: per mode the sketch
+// (K1) + fixed-order split-K reduction, the NCCL sum of the Y partial when the
+// tensor is sharded, the CholQR2 (K4) and the shrink (K2).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/trg.h"
+#include "host_solve.hpp"
+#include "kernels.h"
+
+namespace {
+
+using trg::F32;
+using trg::F64;
+
+thread_local std::string g_err;
+
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct nccl_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct nodev_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+void require(bool ok, const std::string& msg) {
+    if (!ok) throw std::invalid_argument(msg);
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return TRG_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return TRG_EINVAL;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return TRG_ERANGE;
+    } catch (const nodev_error& e) {
+        g_err = e.what();
+        return TRG_ENODEV;
+    } catch (const cuda_error& e) {
+        g_err = e.what();
+        return TRG_ECUDA;
+    } catch (const nccl_error& e) {
+        g_err = e.what();
+        return TRG_ENCCL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TRG_EINTERNAL;
+    }
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+    void load() {
+        if (h) return;
+        // prefer an already-loaded NCCL (e.g. torch's) so one copy serves the process
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) throw nccl_error("NCCL (libnccl.so.2) not loadable");
+        getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+        commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+        getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+        if (!getUniqueId || !commInitRank || !commDestroy || !allReduce)
+            throw nccl_error("NCCL symbols missing");
+    }
+    void check(ncclResult_t r, const char* what) {
+        if (r != ncclSuccess)
+            throw nccl_error(std::string(what) + ": " + (getErrorString ? getErrorString(r) : "nccl error"));
+    }
+};
+Nccl& nccl() {
+    static Nccl n;
+    return n;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct KStat {
+    double ms = 0.0;
+    int64_t n = 0;
+};
+
+struct trg_ctx {
+    int device = 0;
+    int rank = 0, world = 1;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    bool profiling = false;
+    int64_t launches = 0;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> event_pool;
+    std::map<std::string, KStat> stats;
+
+    cudaEvent_t get_event() {
+        if (!event_pool.empty()) {
+            cudaEvent_t e = event_pool.back();
+            event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
+    // Run one kernel launch, counted and (optionally) timed with events on the stream.
+    template <typename F>
+    void launch(const std::string& label, F&& f, int count = 1) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (profiling) {
+            a = get_event();
+            b = get_event();
+            CK(cudaEventRecord(a, stream));
+        }
+        f();
+        CK(cudaGetLastError());
+        launches += count;
+        if (profiling) {
+            CK(cudaEventRecord(b, stream));
+            pending.push_back({label, {a, b}});
+        }
+    }
+    void collect() {
+        if (pending.empty()) return;
+        CK(cudaStreamSynchronize(stream));
+        for (auto& p : pending) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+            KStat& s = stats[p.first];
+            s.ms += ms;
+            s.n += 1;
+            event_pool.push_back(p.second.first);
+            event_pool.push_back(p.second.second);
+        }
+        pending.clear();
+    }
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        if (bytes == 0) bytes = 8;
+        CK(cudaMallocAsync(&p, bytes, stream));
+        return p;
+    }
+    void dfree(void* p) {
+        if (p) cudaFreeAsync(p, stream);
+    }
+    void allreduce(void* buf, size_t count, int dtype) {
+        if (world == 1 || count == 0) return;
+        nccl().check(nccl().allReduce(buf, buf, count, dtype == F64 ? ncclFloat64 : ncclFloat32, ncclSum, comm, stream),
+                     "ncclAllReduce");
+    }
+    void allreduce_op(void* buf, size_t count, ncclRedOp_t op) {
+        if (world == 1 || count == 0) return;
+        nccl().check(nccl().allReduce(buf, buf, count, ncclFloat64, op, comm, stream), "ncclAllReduce");
+    }
+};
+
+struct trg_tensor {
+    trg_ctx* ctx = nullptr;
+    int dtype = F64;
+    std::vector<int64_t> dims;  // global
+    int64_t lo = 0, hi = 0;     // local slab of the last mode
+    void* d = nullptr;
+    int64_t local_elems = 0;
+    std::vector<int64_t> local_shape() const {
+        std::vector<int64_t> s = dims;
+        s.back() = hi - lo;
+        return s;
+    }
+    int64_t inner() const {  // prod of all but the last mode
+        int64_t p = 1;
+        for (size_t i = 0; i + 1 < dims.size(); ++i) p *= dims[i];
+        return p;
+    }
+};
+
+struct trg_sketch {
+    trg_ctx* ctx = nullptr;
+    int dtype = F64;
+    int variant = TRG_SEQUENTIAL;
+    std::vector<int64_t> dims, K;
+    std::vector<double*> dQ;  // device Q_n (nullptr for skipped modes)
+    std::vector<double*> dY;  // device Y_n full rows
+    int* dflags = nullptr;
+    void* dP = nullptr;       // device P (dtype), full prod K
+    bool P_is_view = false;   // P aliases x (no mode projected, unsharded)
+    int64_t P_elems = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ~trg_sketch() {
+        if (!ctx) return;
+        for (double* p : dQ) ctx->dfree(p);
+        for (double* p : dY) ctx->dfree(p);
+        ctx->dfree(dflags);
+        if (!P_is_view) ctx->dfree(dP);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+};
+
+struct trg_report {
+    std::vector<int64_t> ranks;
+    std::vector<double> cores;
+    std::vector<double> rse_history;
+    std::vector<double> projected;
+    int64_t sweeps = 0;
+    double ms[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace {
+
+int64_t prod(const std::vector<int64_t>& v, size_t b = 0, size_t e = SIZE_MAX) {
+    int64_t p = 1;
+    for (size_t i = b; i < std::min(e, v.size()); ++i) p *= v[i];
+    return p;
+}
+
+void shard(int64_t extent, int rank, int world, int64_t& lo, int64_t& hi) {
+    const int64_t base = extent / world, rem = extent % world;
+    lo = rank * base + std::min<int64_t>(rank, rem);
+    hi = lo + base + (rank < rem ? 1 : 0);
+}
+
+void ensure_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) throw nodev_error("no CUDA device available (libtrg has no CPU fallback)");
+}
+
+void validate_K(const trg_tensor* x, const int64_t* K) {
+    require(K != nullptr, "sketch: projection size list must match tensor order");
+    for (size_t n = 0; n < x->dims.size(); ++n)
+        require(K[n] >= 1 && K[n] <= x->dims[n], "sketch: need 1 <= K_n <= I_n in mode " + std::to_string(n));
+}
+
+// ------------------------------------------------------------------ projection pipeline
+// Y_n of the (local) current tensor cur with shape cur_shape, into dYfull
+// (I_n x K_n, replicated). Returns the rows_glob of Omega_n.
+int64_t sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
+                    int64_t Kn, uint64_t seed, uint64_t D, double* dYfull) {
+    const int N = (int)cur_shape.size();
+    const int64_t local_last = x->hi - x->lo;
+    trg::SketchPlan p{};
+    p.dtype = x->dtype;
+    p.left = prod(cur_shape, 0, n);
+    p.dim = cur_shape[n];
+    p.right = prod(cur_shape, n + 1);
+    p.K = (int)Kn;
+    p.seed = seed;
+    p.D = D;
+    if (n < N - 1) {
+        const int64_t r_inner = p.right / local_last;  // prod of modes n+1..N-2
+        p.rows_glob = p.left * r_inner * x->dims[N - 1];
+        p.col_off = p.left * r_inner * x->lo;
+    } else {
+        p.rows_glob = p.left;  // last mode: columns are l only
+        p.col_off = 0;
+    }
+    trg::plan_sketch(p, ctx->num_sms);
+    double* partial = (double*)ctx->alloc(p.partial_elems * sizeof(double));
+    const bool sharded_rows = (n == N - 1) && ctx->world > 1;
+    double* ylocal = sharded_rows ? (double*)ctx->alloc(sizeof(double) * p.dim * Kn) : dYfull;
+    ctx->launch("sketch_m" + std::to_string(n), [&] { trg::launch_sketch(p, cur, partial, ylocal, ctx->stream); }, 2);
+    ctx->dfree(partial);
+    if (sharded_rows) {
+        ctx->launch("scatter", [&] {
+            trg::launch_scatter_rows(ylocal, p.dim, (int)Kn, x->lo, x->dims[n], dYfull, ctx->stream);
+        });
+        ctx->dfree(ylocal);
+    }
+    ctx->allreduce(dYfull, (size_t)(x->dims[n] * Kn), F64);
+    return p.rows_glob;
+}
+
+// out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
+void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
+                  int64_t Kn, const double* dQ) {
+    const int N = (int)cur_shape.size();
+    trg::TTMPlan p{};
+    p.dtype = x->dtype;
+    p.left = prod(cur_shape, 0, n);
+    p.dim = cur_shape[n];
+    p.right = prod(cur_shape, n + 1);
+    p.odim = Kn;
+    p.m_so = x->dims[n];  // M(o=k, d) = Q[d + I_n*k]
+    p.m_sd = 1;
+    const double* m = dQ;
+    if (n == N - 1) m += x->lo;  // local rows of Q_{N-1}
+    trg::plan_ttm(p, ctx->num_sms);
+    const size_t es = trg::dtype_size(x->dtype);
+    void* out = ctx->alloc(es * (size_t)(p.left * Kn * p.right));
+    ctx->launch("ttm_m" + std::to_string(n), [&] { trg::launch_ttm(p, cur, out, m, ctx->stream); });
+    return out;
+}
+
+void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk) {
+    const int N = (int)x->dims.size();
+    validate_K(x, Kin);
+    require(variant == TRG_SEQUENTIAL || variant == TRG_FUSED, "sketch: unknown variant");
+    sk->ctx = ctx;
+    sk->dtype = x->dtype;
+    sk->variant = variant;
+    sk->dims = x->dims;
+    sk->K.assign(Kin, Kin + N);
+    sk->dQ.assign(N, nullptr);
+    sk->dY.assign(N, nullptr);
+    CK(cudaEventCreate(&sk->ev0));
+    CK(cudaEventCreate(&sk->ev1));
+    CK(cudaEventRecord(sk->ev0, ctx->stream));
+    sk->dflags = (int*)ctx->alloc(sizeof(int) * N);
+    CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * N, ctx->stream));
+
+    const size_t es = trg::dtype_size(x->dtype);
+    std::vector<int64_t> shape = x->local_shape();
+    const void* cur = x->d;
+    void* owned = nullptr;  // buffer owned by the pipeline (not x)
+    uint64_t D = 0;         // stream offset: draws consumed by earlier modes (sketch.hpp:69)
+
+    auto qr = [&](int n) {
+        const int64_t In = x->dims[n], Kn = sk->K[n];
+        double* work = (double*)ctx->alloc(sizeof(double) * In * Kn);
+        sk->dQ[n] = (double*)ctx->alloc(sizeof(double) * In * Kn);
+        ctx->launch("qr", [&] { trg::launch_qr(sk->dY[n], In, (int)Kn, sk->dQ[n], work, sk->dflags + n, ctx->stream); });
+        ctx->dfree(work);
+    };
+
+    if (variant == TRG_SEQUENTIAL) {
+        for (int n = 0; n < N; ++n) {
+            const int64_t Kn = sk->K[n];
+            if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
+            sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
+            const int64_t rows_glob = sketch_mode(ctx, x, cur, shape, n, Kn, seed, D, sk->dY[n]);
+            D += (uint64_t)rows_glob * (uint64_t)Kn;
+            qr(n);
+            void* out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
+            if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), x->dtype);
+            if (owned) ctx->dfree(owned);
+            owned = out;
+            cur = out;
+            shape[n] = Kn;
+        }
+    } else {
+        // all Y_n from the original X, Omega_n sized against X,
+        // one stream in mode order; then the shrink chain.
+        std::vector<int64_t> xshape = x->local_shape();
+        for (int n = 0; n < N; ++n) {
+            const int64_t Kn = sk->K[n];
+            if (Kn == x->dims[n]) continue;
+            sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
+            const int64_t rows_glob = sketch_mode(ctx, x, x->d, xshape, n, Kn, seed, D, sk->dY[n]);
+            D += (uint64_t)rows_glob * (uint64_t)Kn;
+            qr(n);
+        }
+        for (int n = 0; n < N; ++n) {
+            const int64_t Kn = sk->K[n];
+            if (Kn == x->dims[n]) continue;
+            void* out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
+            if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), x->dtype);
+            if (owned) ctx->dfree(owned);
+            owned = out;
+            cur = out;
+            shape[n] = Kn;
+        }
+    }
+    const bool last_projected = sk->K[N - 1] != x->dims[N - 1];
+    if (ctx->world > 1 && !last_projected) {
+        // P still sharded along the last mode: zero-padded gather by allreduce
+        const int64_t inner = prod(shape, 0, N - 1);
+        const int64_t full = inner * x->dims[N - 1];
+        void* g = ctx->alloc(es * full);
+        CK(cudaMemsetAsync(g, 0, es * full, ctx->stream));
+        CK(cudaMemcpyAsync((char*)g + es * inner * x->lo, cur, es * inner * (x->hi - x->lo), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+        ctx->allreduce(g, (size_t)full, x->dtype);
+        if (owned) ctx->dfree(owned);
+        owned = g;
+        cur = g;
+        shape[N - 1] = x->dims[N - 1];
+    }
+    sk->P_elems = prod(shape);
+    if (owned) {
+        sk->dP = owned;
+        sk->P_is_view = false;
+    } else {
+        sk->dP = const_cast<void*>(cur);  // no mode projected: P is x itself (sketch.hpp:71)
+        sk->P_is_view = true;
+    }
+    CK(cudaEventRecord(sk->ev1, ctx->stream));
+}
+
+void download_P(const trg_sketch* sk, std::vector<double>& out) {
+    trg_ctx* ctx = sk->ctx;
+    out.resize((size_t)sk->P_elems);
+    if (sk->dtype == F64) {
+        CK(cudaMemcpyAsync(out.data(), sk->dP, sizeof(double) * sk->P_elems, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+        std::vector<float> tmp((size_t)sk->P_elems);
+        CK(cudaMemcpyAsync(tmp.data(), sk->dP, sizeof(float) * sk->P_elems, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (size_t i = 0; i < tmp.size(); ++i) out[i] = tmp[i];
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+
+void download_basis(const trg_sketch* sk, int n, double* out) {
+    const int64_t In = sk->dims[n], Kn = sk->K[n];
+    if (!sk->dQ[n]) {
+        for (int64_t j = 0; j < Kn; ++j)
+            for (int64_t i = 0; i < In; ++i) out[i + In * j] = (i == j) ? 1.0 : 0.0;
+        return;
+    }
+    CK(cudaMemcpyAsync(out, sk->dQ[n], sizeof(double) * In * Kn, cudaMemcpyDeviceToHost, sk->ctx->stream));
+    CK(cudaStreamSynchronize(sk->ctx->stream));
+}
+
+// ------------------------------------------------------------------ TR model on device
+// cores (flat) -> per-core host vectors
+std::vector<std::vector<double>> split_cores(int N, const int64_t* dims, const int64_t* ranks, const double* cores) {
+    std::vector<std::vector<double>> out;
+    const double* p = cores;
+    for (int n = 0; n < N; ++n) {
+        const int64_t sz = ranks[n] * dims[n] * ranks[(n + 1) % N];
+        out.emplace_back(p, p + sz);
+        p += sz;
+    }
+    return out;
+}
+
+// Subchain S = G_1 o ... o G_{N-1} over the local slab [lo, hi) of the last mode,
+// shape (R_1, P_local, R_0), on device. Caller frees.
+double* device_subchain(trg_ctx* ctx, int N, const int64_t* dims, const int64_t* ranks,
+                        const std::vector<std::vector<double>>& cs, int64_t lo, int64_t hi, int64_t& P_local) {
+    auto upload = [&](const std::vector<double>& v) {
+        double* d = (double*)ctx->alloc(sizeof(double) * v.size());
+        CK(cudaMemcpyAsync(d, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, ctx->stream));
+        return d;
+    };
+    auto last_slab = [&](int n) {
+        // core n restricted to middle indices [lo, hi): (R, hi-lo, R')
+        const int64_t r = ranks[n], I = dims[n], rp = ranks[(n + 1) % N];
+        std::vector<double> v((size_t)(r * (hi - lo) * rp));
+        for (int64_t s = 0; s < rp; ++s)
+            for (int64_t i = lo; i < hi; ++i)
+                for (int64_t a = 0; a < r; ++a) v[a + r * ((i - lo) + (hi - lo) * s)] = cs[n][a + r * (i + I * s)];
+        return v;
+    };
+    auto core_host = [&](int n) { return n == N - 1 ? last_slab(n) : cs[n]; };
+    auto mid = [&](int n) { return n == N - 1 ? hi - lo : dims[n]; };
+    double* cur = upload(core_host(1));
+    int64_t ra = ranks[1], p = mid(1), rb = ranks[2 % N];
+    for (int k = 2; k < N; ++k) {
+        const std::vector<double> gh = core_host(k);
+        double* g = upload(gh);
+        const int64_t i = mid(k), rc = ranks[(k + 1) % N];
+        double* out = (double*)ctx->alloc(sizeof(double) * ra * p * i * rc);
+        ctx->launch("chain", [&] { trg::launch_chain(cur, ra, p, rb, g, i, rc, out, ctx->stream); });
+        ctx->dfree(cur);
+        ctx->dfree(g);
+        cur = out;
+        p *= i;
+        rb = rc;
+    }
+    P_local = p;
+    return cur;
+}
+
+// Reconstruct (write_mode = 1: X := Xhat) or accumulate the RSE sums (0) over the local slab.
+void device_recon(trg_ctx* ctx, trg_tensor* x, const int64_t* ranks, const double* cores, int write_mode,
+                  double* host_sums) {
+    const int N = (int)x->dims.size();
+    require(N >= 2, "device reconstruction needs order >= 2");
+    const auto cs = split_cores(N, x->dims.data(), ranks, cores);
+    int64_t P_local = 0;
+    double* S = device_subchain(ctx, N, x->dims.data(), ranks, cs, x->lo, x->hi, P_local);
+    double* g0 = (double*)ctx->alloc(sizeof(double) * cs[0].size());
+    CK(cudaMemcpyAsync(g0, cs[0].data(), sizeof(double) * cs[0].size(), cudaMemcpyHostToDevice, ctx->stream));
+    trg::ReconPlan rp{};
+    rp.dtype = x->dtype;
+    rp.I0 = x->dims[0];
+    rp.P = P_local;
+    rp.R0 = ranks[0];
+    rp.R1 = ranks[1 % N];
+    trg::plan_recon(rp, ctx->num_sms);
+    double* bs = write_mode ? nullptr : (double*)ctx->alloc(sizeof(double) * 2 * rp.nblocks);
+    ctx->launch(write_mode ? "synth" : "rse", [&] { trg::launch_recon(rp, g0, S, x->d, write_mode, bs, ctx->stream); });
+    if (!write_mode) {
+        double* sums = (double*)ctx->alloc(sizeof(double) * 2);
+        ctx->launch("rse_sum", [&] { trg::launch_sum_pairs(bs, rp.nblocks, sums, ctx->stream); });
+        ctx->allreduce(sums, 2, F64);
+        CK(cudaMemcpyAsync(host_sums, sums, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->dfree(sums);
+        ctx->dfree(bs);
+    }
+    ctx->dfree(S);
+    ctx->dfree(g0);
+}
+
+double rse_device(trg_ctx* ctx, const trg_tensor* x, const int64_t* ranks, const double* cores) {
+    const int N = (int)x->dims.size();
+    for (int n = 0; n < N; ++n) require(ranks[n] >= 1, "rse: ranks must be positive");
+    if (N == 1) {
+        // X(i) = trace(G(:, i, :)) — order-one tensors are tiny: host evaluation
+        std::vector<double> xh((size_t)x->local_elems);
+        trg_tensor_download(x, xh.data());
+        const int64_t r = ranks[0], I = x->dims[0];
+        double num = 0.0, den = 0.0;
+        for (int64_t i = 0; i < I; ++i) {
+            double tr = 0.0;
+            for (int64_t a = 0; a < r; ++a) tr += cores[a + r * (i + I * a)];
+            num += (xh[i] - tr) * (xh[i] - tr);
+            den += xh[i] * xh[i];
+        }
+        require(den > 0.0, "rse: reference tensor has zero norm");
+        return std::sqrt(num) / std::sqrt(den);
+    }
+    double sums[2];
+    device_recon(ctx, const_cast<trg_tensor*>(x), ranks, cores, 0, sums);
+    require(sums[1] > 0.0, "rse: reference tensor has zero norm");
+    return std::sqrt(sums[0]) / std::sqrt(sums[1]);
+}
+
+void back_project_device(trg_ctx* ctx, int N, const int64_t* K, const int64_t* ranks, const double* small,
+                         const trg_sketch* sk, double* out) {
+    require((int)sk->dims.size() == N, "back_project: need one basis per core");
+    const double* zp = small;
+    double* op = out;
+    for (int n = 0; n < N; ++n) {
+        require(K[n] == sk->K[n], "back_project: basis/core dimension mismatch in mode " + std::to_string(n));
+        const int64_t r = ranks[n], rn = ranks[(n + 1) % N], In = sk->dims[n];
+        const int64_t zsz = r * K[n] * rn, osz = r * In * rn;
+        if (!sk->dQ[n]) {  // identity basis: bit-exact copy (sketch.hpp:115-118)
+            std::memcpy(op, zp, sizeof(double) * zsz);
+        } else {
+            double* dz = (double*)ctx->alloc(sizeof(double) * zsz);
+            double* dg = (double*)ctx->alloc(sizeof(double) * osz);
+            CK(cudaMemcpyAsync(dz, zp, sizeof(double) * zsz, cudaMemcpyHostToDevice, ctx->stream));
+            trg::TTMPlan p{};
+            p.dtype = F64;
+            p.left = r;
+            p.dim = K[n];
+            p.right = rn;
+            p.odim = In;
+            p.m_so = 1;  // M(o=i, d=k) = Q[i + I_n*k]
+            p.m_sd = In;
+            trg::plan_ttm(p, ctx->num_sms);
+            ctx->launch("back_project", [&] { trg::launch_ttm(p, dz, dg, sk->dQ[n], ctx->stream); });
+            CK(cudaMemcpyAsync(op, dg, sizeof(double) * osz, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            ctx->dfree(dz);
+            ctx->dfree(dg);
+        }
+        zp += zsz;
+        op += osz;
+    }
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void decompose_impl(trg_ctx* ctx, const trg_tensor* x, int method, const int64_t* ranks, double tol,
+                    int64_t max_sweeps, uint64_t cfg_seed, const int64_t* K, uint64_t spec_seed, int variant,
+                    trg_report* rep, double t_start) {
+    const int N = (int)x->dims.size();
+    require(method == TRG_ALS || method == TRG_SVD, "decompose: unknown method");
+    validate_K(x, K);  // validated before the rank warning (reference quirk sketch.hpp:131-138 fixed)
+    const char* who = method == TRG_ALS ? "rtrals" : "rtrsvd";
+    if (method == TRG_ALS) {
+        require(ranks != nullptr, "trals: rank vector required");
+        for (int n = 0; n < N; ++n) require(ranks[n] >= 1, "trals: ranks must be positive");
+        require(max_sweeps >= 1, "trals: max_sweeps must be positive");
+    } else {
+        require(tol >= 0.0, "trsvd: tolerance must be nonnegative");
+    }
+    if (ranks && ctx->rank == 0)
+        for (int n = 0; n < N; ++n)
+            if (ranks[n] > K[n])
+                std::cerr << who << ": warning: rank " << ranks[n] << " exceeds projection size " << K[n]
+                          << " in mode " << n << "\n";
+    double t0 = now_ms();
+    trg_sketch sk;
+    run_sketch(ctx, x, K, spec_seed, variant, &sk);
+    trg::host::Tensor P;
+    P.shape.assign(K, K + N);
+    download_P(&sk, P.data);
+    double t1 = now_ms();
+    rep->ms[1] = t1 - t0;
+    rep->projected = P.data;
+    trg::host::SolveOut inner;
+    if (method == TRG_ALS)
+        inner = trg::host::trals(P, std::vector<int64_t>(ranks, ranks + N), tol, max_sweeps, cfg_seed);
+    else
+        inner = trg::host::trsvd(P, tol);
+    double t2 = now_ms();
+    rep->ms[2] = t2 - t1;
+    std::vector<int64_t> rk(N);
+    std::vector<double> small;
+    for (int n = 0; n < N; ++n) {
+        rk[n] = inner.cores.rank(n);
+        const auto& g = inner.cores.g[n].data;
+        small.insert(small.end(), g.begin(), g.end());
+    }
+    int64_t total = 0;
+    for (int n = 0; n < N; ++n) total += rk[n] * x->dims[n] * rk[(n + 1) % N];
+    rep->cores.assign((size_t)total, 0.0);
+    back_project_device(ctx, N, K, rk.data(), small.data(), &sk, rep->cores.data());
+    double t3 = now_ms();
+    rep->ms[3] = t3 - t2;
+    rep->rse_history = inner.rse_history;
+    rep->rse_history.push_back(rse_device(ctx, x, rk.data(), rep->cores.data()));
+    double t4 = now_ms();
+    rep->ms[4] = t4 - t3;
+    rep->ranks = rk;
+    rep->sweeps = inner.sweeps_run;
+    rep->ms[5] = t4 - t_start;
+}
+
+trg_tensor* tensor_new(trg_ctx* ctx, int dtype, int order, const int64_t* dims) {
+    require(ctx != nullptr, "tensor: null context");
+    require(dtype == F32 || dtype == F64, "tensor: dtype must be TRG_F32 or TRG_F64");
+    require(order >= 1, "DenseTensor: order must be at least 1");
+    for (int n = 0; n < order; ++n) require(dims[n] >= 1, "DenseTensor: every extent must be positive");
+    auto t = std::make_unique<trg_tensor>();
+    t->ctx = ctx;
+    t->dtype = dtype;
+    t->dims.assign(dims, dims + order);
+    shard(t->dims.back(), ctx->rank, ctx->world, t->lo, t->hi);
+    require(t->hi > t->lo, "tensor: last mode extent smaller than the number of ranks");
+    t->local_elems = t->inner() * (t->hi - t->lo);
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMalloc(&t->d, trg::dtype_size(dtype) * (size_t)t->local_elems));
+    return t.release();
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int trg_abi_version(void) { return TRG_ABI_VERSION; }
+const char* trg_last_error(void) { return g_err.c_str(); }
+
+int trg_device_count(int* count) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+        cudaGetLastError();
+        *count = n;
+    });
+}
+
+int trg_shard_range(int64_t extent, int rank, int world, int64_t* lo, int64_t* hi) {
+    return guard([&] {
+        require(world >= 1 && rank >= 0 && rank < world, "shard: bad rank/world");
+        require(extent >= 1, "shard: extent must be positive");
+        shard(extent, rank, world, *lo, *hi);
+    });
+}
+
+static void ctx_init(trg_ctx* c, int device) {
+    ensure_device();
+    CK(cudaSetDevice(device));
+    c->device = device;
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) throw nodev_error("libtrg is built for sm_100a (B200); device has compute capability major " +
+                                       std::to_string(major));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+}
+
+int trg_ctx_create(int device, trg_ctx** out) {
+    return guard([&] {
+        auto c = std::make_unique<trg_ctx>();
+        ctx_init(c.get(), device);
+        *out = c.release();
+    });
+}
+
+int trg_nccl_unique_id(unsigned char id[128]) {
+    return guard([&] {
+        nccl().load();
+        ncclUniqueId u;
+        nccl().check(nccl().getUniqueId(&u), "ncclGetUniqueId");
+        std::memcpy(id, u.internal, 128);
+    });
+}
+
+int trg_ctx_create_dist(int device, int rank, int world, const unsigned char id[128], trg_ctx** out) {
+    return guard([&] {
+        require(world >= 1 && rank >= 0 && rank < world, "ctx: bad rank/world");
+        auto c = std::make_unique<trg_ctx>();
+        ctx_init(c.get(), device);
+        c->rank = rank;
+        c->world = world;
+        if (world > 1) {
+            nccl().load();
+            ncclUniqueId u;
+            std::memcpy(u.internal, id, 128);
+            nccl().check(nccl().commInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+        }
+        *out = c.release();
+    });
+}
+
+int trg_ctx_destroy(trg_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& p : ctx->pending) {
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        for (auto e : ctx->event_pool) cudaEventDestroy(e);
+        if (ctx->comm) nccl().commDestroy(ctx->comm);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int trg_ctx_synchronize(trg_ctx* ctx) { return guard([&] { CK(cudaStreamSynchronize(ctx->stream)); }); }
+int trg_ctx_stream(trg_ctx* ctx, void** s) { return guard([&] { *s = (void*)ctx->stream; }); }
+int trg_ctx_set_profiling(trg_ctx* ctx, int on) {
+    return guard([&] {
+        ctx->collect();
+        ctx->profiling = on != 0;
+    });
+}
+int trg_ctx_kernel_stats(trg_ctx* ctx, const char* label, double* total_ms, int64_t* launches) {
+    return guard([&] {
+        ctx->collect();
+        double ms = 0.0;
+        int64_t n = 0;
+        for (auto& kv : ctx->stats)
+            if (!label || kv.first == label) {
+                ms += kv.second.ms;
+                n += kv.second.n;
+            }
+        if (total_ms) *total_ms = ms;
+        if (launches) *launches = n;
+    });
+}
+int trg_ctx_kernel_labels(trg_ctx* ctx, char* buf, int64_t cap) {
+    return guard([&] {
+        ctx->collect();
+        std::string s;
+        for (auto& kv : ctx->stats) s += kv.first + "\n";
+        require((int64_t)s.size() < cap, "labels: buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+int trg_ctx_launch_count(trg_ctx* ctx, int64_t* n) { return guard([&] { *n = ctx->launches; }); }
+int trg_ctx_reset_stats(trg_ctx* ctx) {
+    return guard([&] {
+        ctx->collect();
+        ctx->stats.clear();
+        ctx->launches = 0;
+    });
+}
+
+int trg_tensor_create(trg_ctx* ctx, int dtype, int order, const int64_t* dims, trg_tensor** out) {
+    return guard([&] { *out = tensor_new(ctx, dtype, order, dims); });
+}
+
+int trg_tensor_info(const trg_tensor* t, int* dtype, int* order, int64_t* dims, int64_t* lo, int64_t* hi) {
+    return guard([&] {
+        if (dtype) *dtype = t->dtype;
+        if (order) *order = (int)t->dims.size();
+        if (dims) std::copy(t->dims.begin(), t->dims.end(), dims);
+        if (lo) *lo = t->lo;
+        if (hi) *hi = t->hi;
+    });
+}
+
+int trg_tensor_upload(trg_tensor* t, const void* host) {
+    return guard([&] {
+        CK(cudaMemcpyAsync(t->d, host, trg::dtype_size(t->dtype) * t->local_elems, cudaMemcpyHostToDevice,
+                           t->ctx->stream));
+        CK(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
+int trg_tensor_download(const trg_tensor* t, void* host) {
+    return guard([&] {
+        CK(cudaMemcpyAsync(host, t->d, trg::dtype_size(t->dtype) * t->local_elems, cudaMemcpyDeviceToHost,
+                           t->ctx->stream));
+        CK(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
+int trg_tensor_device_ptr(const trg_tensor* t, void** ptr, int64_t* n) {
+    return guard([&] {
+        *ptr = t->d;
+        if (n) *n = t->local_elems;
+    });
+}
+
+int trg_tensor_synthesize(trg_tensor* t, const int64_t* ranks, const double* cores, int rescale01, double snr_db,
+                          uint64_t noise_seed) {
+    return guard([&] {
+        trg_ctx* ctx = t->ctx;
+        const int N = (int)t->dims.size();
+        require(N >= 2, "synthesize: order must be at least 2");
+        device_recon(ctx, t, ranks, cores, 1, nullptr);
+        const int nb = std::min<int64_t>(1024, (t->local_elems + 255) / 256);
+        double* bs = (double*)ctx->alloc(sizeof(double) * 2 * nb);
+        double* sums = (double*)ctx->alloc(sizeof(double) * 2);
+        double h[2];
+        if (rescale01) {
+            ctx->launch("minmax", [&] { trg::launch_minmax(t->d, t->dtype, t->local_elems, bs, nb, ctx->stream); });
+            std::vector<double> hb(2 * nb);
+            CK(cudaMemcpyAsync(hb.data(), bs, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            double lo = 1e308, hi = -1e308;
+            for (int i = 0; i < nb; ++i) {
+                lo = std::min(lo, hb[2 * i]);
+                hi = std::max(hi, hb[2 * i + 1]);
+            }
+            h[0] = -lo;
+            h[1] = hi;
+            CK(cudaMemcpyAsync(sums, h, sizeof(double) * 2, cudaMemcpyHostToDevice, ctx->stream));
+            ctx->allreduce_op(sums, 2, ncclMax);
+            CK(cudaMemcpyAsync(h, sums, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            lo = -h[0];
+            hi = h[1];
+            if (hi > lo) ctx->launch("affine", [&] {
+                trg::launch_affine(t->d, t->dtype, t->local_elems, 1.0 / (hi - lo), -lo / (hi - lo), ctx->stream);
+            });
+        }
+        if (std::isfinite(snr_db)) {
+            const uint64_t off = (uint64_t)(t->inner() * t->lo);  // global flat index of the slab
+            ctx->launch("noise_norms", [&] {
+                trg::launch_noise_norms(t->d, t->dtype, t->local_elems, noise_seed, off, bs, nb, ctx->stream);
+            });
+            ctx->launch("noise_sum", [&] { trg::launch_sum_pairs(bs, nb, sums, ctx->stream); });
+            ctx->allreduce(sums, 2, F64);
+            CK(cudaMemcpyAsync(h, sums, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            require(h[0] > 0.0, "add_noise: zero-norm input");
+            const double alpha = std::sqrt(h[0]) * std::pow(10.0, -snr_db / 20.0) / std::sqrt(h[1]);
+            ctx->launch("add_noise", [&] {
+                trg::launch_add_noise(t->d, t->dtype, t->local_elems, noise_seed, off, alpha, ctx->stream);
+            });
+        }
+        ctx->dfree(bs);
+        ctx->dfree(sums);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int trg_tensor_destroy(trg_tensor* t) {
+    return guard([&] {
+        if (!t) return;
+        cudaStreamSynchronize(t->ctx->stream);
+        cudaFree(t->d);
+        delete t;
+    });
+}
+
+int trg_sketch_run(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t seed, int variant,
+                   trg_sketch** out) {
+    return guard([&] {
+        require(ctx && x, "sketch: null argument");
+        auto sk = std::make_unique<trg_sketch>();
+        run_sketch(ctx, x, K, seed, variant, sk.get());
+        *out = sk.release();
+    });
+}
+
+int trg_sketch_projected(const trg_sketch* sk, double* out) {
+    return guard([&] {
+        std::vector<double> p;
+        download_P(sk, p);
+        std::memcpy(out, p.data(), sizeof(double) * p.size());
+    });
+}
+
+int trg_sketch_basis(const trg_sketch* sk, int mode, double* out) {
+    return guard([&] {
+        if (mode < 0 || mode >= (int)sk->dims.size())
+            throw std::out_of_range("DenseTensor: mode " + std::to_string(mode) + " out of range");
+        download_basis(sk, mode, out);
+    });
+}
+
+int trg_sketch_y(const trg_sketch* sk, int mode, double* out) {
+    return guard([&] {
+        if (mode < 0 || mode >= (int)sk->dims.size())
+            throw std::out_of_range("DenseTensor: mode " + std::to_string(mode) + " out of range");
+        const int64_t n = sk->dims[mode] * sk->K[mode];
+        if (!sk->dY[mode]) {
+            std::fill(out, out + n, 0.0);
+            return;
+        }
+        CK(cudaMemcpyAsync(out, sk->dY[mode], sizeof(double) * n, cudaMemcpyDeviceToHost, sk->ctx->stream));
+        CK(cudaStreamSynchronize(sk->ctx->stream));
+    });
+}
+
+int trg_sketch_qr_path(const trg_sketch* sk, int mode, int* hh) {
+    return guard([&] {
+        if (mode < 0 || mode >= (int)sk->dims.size()) throw std::out_of_range("mode out of range");
+        int v = 0;
+        CK(cudaMemcpyAsync(&v, sk->dflags + mode, sizeof(int), cudaMemcpyDeviceToHost, sk->ctx->stream));
+        CK(cudaStreamSynchronize(sk->ctx->stream));
+        *hh = v;
+    });
+}
+
+int trg_sketch_elapsed_ms(const trg_sketch* sk, double* ms) {
+    return guard([&] {
+        CK(cudaEventSynchronize(sk->ev1));
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, sk->ev0, sk->ev1));
+        *ms = f;
+    });
+}
+
+int trg_sketch_destroy(trg_sketch* sk) {
+    return guard([&] { delete sk; });
+}
+
+int trg_omega(trg_ctx* ctx, uint64_t seed, uint64_t offset, int64_t rows, int64_t cols, double* out) {
+    return guard([&] {
+        require(rows >= 1 && cols >= 1, "gaussian_matrix: dimensions must be positive");
+        double* d = (double*)ctx->alloc(sizeof(double) * rows * cols);
+        ctx->launch("omega", [&] { trg::launch_omega(seed, offset, rows, cols, d, ctx->stream); });
+        CK(cudaMemcpyAsync(out, d, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->dfree(d);
+    });
+}
+
+int trg_mode_n_product(trg_ctx* ctx, const trg_tensor* x, int mode, int64_t m_rows, const double* m,
+                       trg_tensor** out) {
+    return guard([&] {
+        const int N = (int)x->dims.size();
+        if (mode < 0 || mode >= N) throw std::out_of_range("DenseTensor: mode " + std::to_string(mode) + " out of range");
+        require(ctx->world == 1, "mode_n_product: unsharded tensors only");
+        require(m_rows >= 1, "mode_n_product: inner dimensions do not match");
+        std::vector<int64_t> od = x->dims;
+        od[mode] = m_rows;
+        trg_tensor* o = tensor_new(ctx, x->dtype, N, od.data());
+        const int64_t In = x->dims[mode];
+        double* dm = (double*)ctx->alloc(sizeof(double) * m_rows * In);
+        CK(cudaMemcpyAsync(dm, m, sizeof(double) * m_rows * In, cudaMemcpyHostToDevice, ctx->stream));
+        trg::TTMPlan p{};
+        p.dtype = x->dtype;
+        p.left = prod(x->dims, 0, mode);
+        p.dim = In;
+        p.right = prod(x->dims, mode + 1);
+        p.odim = m_rows;
+        p.m_so = 1;  // M(o, d) = m[o + m_rows*d]
+        p.m_sd = m_rows;
+        trg::plan_ttm(p, ctx->num_sms);
+        ctx->launch("ttm", [&] { trg::launch_ttm(p, x->d, o->d, dm, ctx->stream); });
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->dfree(dm);
+        *out = o;
+    });
+}
+
+int trg_back_project(trg_ctx* ctx, int order, const int64_t* K, const int64_t* ranks, const double* small_cores,
+                     const trg_sketch* sk, double* cores_out) {
+    return guard([&] { back_project_device(ctx, order, K, ranks, small_cores, sk, cores_out); });
+}
+
+int trg_rse(trg_ctx* ctx, const trg_tensor* x, const int64_t* ranks, const double* cores, double* out) {
+    return guard([&] { *out = rse_device(ctx, x, ranks, cores); });
+}
+
+int trg_decompose(trg_ctx* ctx, const trg_tensor* x, int method, const int64_t* ranks, double tol,
+                  int64_t max_sweeps, uint64_t cfg_seed, const int64_t* K, uint64_t spec_seed, int variant,
+                  trg_report** out) {
+    return guard([&] {
+        auto rep = std::make_unique<trg_report>();
+        decompose_impl(ctx, x, method, ranks, tol, max_sweeps, cfg_seed, K, spec_seed, variant, rep.get(), now_ms());
+        *out = rep.release();
+    });
+}
+
+int trg_decompose_host(trg_ctx* ctx, int dtype, int order, const int64_t* dims, const void* host_local, int method,
+                       const int64_t* ranks, double tol, int64_t max_sweeps, uint64_t cfg_seed, const int64_t* K,
+                       uint64_t spec_seed, int variant, trg_report** out) {
+    return guard([&] {
+        const double t0 = now_ms();
+        std::unique_ptr<trg_tensor, void (*)(trg_tensor*)> x(tensor_new(ctx, dtype, order, dims),
+                                                             [](trg_tensor* t) { trg_tensor_destroy(t); });
+        CK(cudaMemcpyAsync(x->d, host_local, trg::dtype_size(dtype) * x->local_elems, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        auto rep = std::make_unique<trg_report>();
+        rep->ms[0] = now_ms() - t0;
+        decompose_impl(ctx, x.get(), method, ranks, tol, max_sweeps, cfg_seed, K, spec_seed, variant, rep.get(), t0);
+        *out = rep.release();
+    });
+}
+
+int trg_report_ranks(const trg_report* r, int64_t* ranks) {
+    return guard([&] { std::copy(r->ranks.begin(), r->ranks.end(), ranks); });
+}
+int trg_report_cores_len(const trg_report* r, int64_t* n) { return guard([&] { *n = (int64_t)r->cores.size(); }); }
+int trg_report_cores(const trg_report* r, double* out) {
+    return guard([&] { std::copy(r->cores.begin(), r->cores.end(), out); });
+}
+int trg_report_rse_history(const trg_report* r, double* out, int64_t* n) {
+    return guard([&] {
+        if (n) *n = (int64_t)r->rse_history.size();
+        if (out) std::copy(r->rse_history.begin(), r->rse_history.end(), out);
+    });
+}
+int trg_report_sweeps(const trg_report* r, int64_t* s) { return guard([&] { *s = r->sweeps; }); }
+int trg_report_timings(const trg_report* r, double* ms) { return guard([&] { std::copy(r->ms, r->ms + 6, ms); }); }
+int trg_report_projected(const trg_report* r, double* out, int64_t* n) {
+    return guard([&] {
+        if (n) *n = (int64_t)r->projected.size();
+        if (out) std::copy(r->projected.begin(), r->projected.end(), out);
+    });
+}
+int trg_report_destroy(trg_report* r) {
+    return guard([&] { delete r; });
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+"""GPU parity: libtrg (sm_100a) against the CPU oracle on identical inputs.
+
+Tolerances (BASELINE.json north_star): fp64 <= 1e-10 relative on Y_n, Q_n, P,
+cores and RSE; fp32 <= 1e-4 relative against the fp64 oracle run on the
+fp32-rounded input. Omega is compared draw by draw.
+"""
+import numpy as np
+import pytest
+
+import oracle_ref as orc
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-10
+F32_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def trg():
+    import paper_1901_01652_b200 as trg
+
+    return trg
+
+
+@pytest.fixture(scope="module")
+def ctx(trg):
+    return trg.default_context()
+
+
+def tr_tensor(dims, ranks, seed, snr=None, scale=1.0):
+    x = orc.reconstruct_full(orc.random_factors(dims, ranks, seed, scale))
+    if snr is not None:
+        x = orc.add_noise(x, snr, seed + 1)
+    return x
+
+
+def relerr(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------------------------------------------------------- RNG
+def test_omega_matches_reference_stream(trg):
+    for seed, off, rows, cols in [(0, 0, 37, 5), (7, 1, 64, 3), (12345, 999, 100, 16), (2**63 + 5, 77, 11, 2)]:
+        got = trg.gaussian_matrix(rows, cols, seed, off)
+        want = orc.gaussian(seed, rows * cols, skip=off).reshape((rows, cols), order="F")
+        np.testing.assert_allclose(got, want, rtol=1e-14, atol=1e-14)
+
+
+# ---------------------------------------------------------------- sketch
+SHAPES = [
+    ((100, 100, 100), (10, 10, 10)),          # C1 shape
+    ((23, 17, 9), (5, 17, 4)),                # odd sizes, mode 1 skipped
+    ((12, 11, 10, 9), (3, 4, 5, 2)),
+    ((8, 7, 6, 5, 4), (2, 3, 6, 2, 3)),       # order 5, mode 2 skipped
+    ((300, 7), (9, 3)),                       # order 2
+    ((129, 33, 65), (17, 8, 64)),             # non-power-of-2 tails, d-tiling
+    ((40,), (6,)),                            # order 1
+    ((6, 5, 4), (6, 5, 4)),                   # all skipped: P = X exactly
+]
+
+
+@pytest.mark.parametrize("dims,K", SHAPES)
+def test_sketch_f64_parity(trg, dims, K):
+    x = np.random.default_rng(sum(dims)).standard_normal(dims)
+    if len(dims) >= 2:
+        x = x + tr_tensor(list(dims), [2] * len(dims), 3)
+    seed = 17
+    proj, bases, ys = orc.sketch(x, K, seed)
+    got = trg.sketch(x, trg.ProjectionSpec(list(K), seed))
+    for n in range(len(dims)):
+        if K[n] == dims[n]:
+            np.testing.assert_array_equal(got.bases[n], np.eye(dims[n]))
+            continue
+        assert relerr(got.sketches[n], ys[n]) < F64_TOL, n
+        assert relerr(got.bases[n], bases[n]) < F64_TOL, n
+        assert np.max(np.abs(got.bases[n].T @ got.bases[n] - np.eye(K[n]))) < 1e-12
+    assert relerr(got.projected, proj) < F64_TOL
+    if all(k == d for k, d in zip(K, dims)):
+        np.testing.assert_array_equal(got.projected, x)  # sketch.hpp:71 identity path
+
+
+@pytest.mark.parametrize("dims,K", SHAPES[:6])
+def test_sketch_f32_parity(trg, dims, K):
+    x = np.random.default_rng(1 + sum(dims)).standard_normal(dims).astype(np.float32)
+    proj, bases, ys = orc.sketch(x.astype(np.float64), K, 5)
+    got = trg.sketch(x, trg.ProjectionSpec(list(K), 5))
+    for n in range(len(dims)):
+        if K[n] != dims[n]:
+            assert relerr(got.sketches[n], ys[n]) < F32_TOL
+            assert relerr(got.bases[n], bases[n]) < F32_TOL
+    assert relerr(got.projected, proj) < F32_TOL
+
+
+def test_sketch_fused_variant_parity(trg):
+    x = tr_tensor([20, 18, 16, 14], [3, 3, 3, 3], 4, snr=30.0)
+    K = [6, 5, 16, 4]
+    proj, bases, ys = orc.sketch(x, K, 9, variant=1)
+    got = trg.sketch(x, trg.ProjectionSpec(K, 9), variant=1)
+    for n in range(4):
+        assert relerr(got.bases[n], bases[n]) < F64_TOL
+    assert relerr(got.projected, proj) < F64_TOL
+
+
+def test_sketch_householder_fallback_matches(trg):
+    # exactly rank-2 unfoldings with K = 5 > rank: Y is rank deficient, CholQR2
+    # must hand over to Householder; the captured range is still exact.
+    rng = np.random.default_rng(3)
+    U = [np.linalg.qr(rng.standard_normal((30, 2)))[0] for _ in range(3)]
+    x = np.einsum("abc,ia,jb,kc->ijk", rng.standard_normal((2, 2, 2)), *U)
+    sk = trg.DeviceSketch(trg.default_context(), trg.DeviceTensor.from_numpy(trg.default_context(), x),
+                          trg.ProjectionSpec([5, 5, 5], 1))
+    res = sk.result()
+    assert res.qr_householder[0] == 1
+    lifted = orc.lift_back(res.projected, res.bases)
+    assert orc.rse(x, lifted) < 1e-8  # SPEC.md:304 exact capture
+
+
+def test_sketch_determinism(trg):
+    x = tr_tensor([50, 40, 30], [3, 3, 3], 8, snr=20.0)
+    a = trg.sketch(x, trg.ProjectionSpec([7, 6, 5], 3))
+    b = trg.sketch(x, trg.ProjectionSpec([7, 6, 5], 3))
+    np.testing.assert_array_equal(a.projected, b.projected)  # SPEC.md:303 bit-identical
+    for qa, qb in zip(a.bases, b.bases):
+        np.testing.assert_array_equal(qa, qb)
+
+
+def test_sketch_errors(trg):
+    x = np.zeros((4, 4, 4))
+    with pytest.raises(ValueError, match="projection size list"):
+        trg.sketch(x, trg.ProjectionSpec([2, 2], 0))
+    with pytest.raises(ValueError, match="1 <= K_n <= I_n in mode 0"):
+        trg.sketch(x, trg.ProjectionSpec([5, 2, 2], 0))
+    with pytest.raises(ValueError, match="in mode 2"):
+        trg.sketch(x, trg.ProjectionSpec([2, 2, 0], 0))
+
+
+# ---------------------------------------------------------------- TTM / back-projection / RSE
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_mode_n_product_parity(trg, dtype):
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((13, 70, 9, 5)).astype(dtype)
+    for mode in range(4):
+        m = rng.standard_normal((7, x.shape[mode]))
+        want = orc.mode_n_product(x.astype(np.float64), mode, m)
+        got = trg.mode_n_product(x, mode, m)
+        assert relerr(got, want) < (F64_TOL if dtype == np.float64 else F32_TOL)
+    with pytest.raises(ValueError):
+        trg.mode_n_product(x, 1, rng.standard_normal((3, 5)))
+    with pytest.raises(IndexError):
+        trg.mode_n_product(x, 4, rng.standard_normal((3, 5)))
+
+
+def test_back_project_parity(trg, ctx):
+    x = tr_tensor([30, 25, 20], [2, 3, 2], 6, snr=25.0)
+    K = [8, 25, 6]
+    spec = trg.ProjectionSpec(K, 2)
+    sk = trg.DeviceSketch(ctx, trg.DeviceTensor.from_numpy(ctx, x), spec)
+    res = sk.result()
+    z = orc.random_factors(K, [2, 3, 4], 9)
+    got = trg.back_project(z, sk)
+    want = orc.back_project(z, res.bases)
+    for n, (a, b) in enumerate(zip(got, want)):
+        if K[n] == x.shape[n]:
+            np.testing.assert_array_equal(a, z[n])  # identity basis: bit-exact copy
+        assert relerr(a, b) < F64_TOL
+
+
+@pytest.mark.parametrize("dims,ranks,dtype", [
+    ([40, 30, 20], [3, 4, 2], np.float64),
+    ([16, 15, 14, 13], [2, 3, 2, 3], np.float64),
+    ([200, 31], [5, 3], np.float64),
+    ([40, 30, 20], [3, 4, 2], np.float32),
+    ([9, 8, 7, 6, 5], [2, 2, 3, 2, 2], np.float64),
+])
+def test_rse_parity(trg, dims, ranks, dtype):
+    x = tr_tensor(dims, ranks, 12, snr=20.0).astype(dtype)
+    cores = orc.random_factors(dims, ranks, 99)
+    want = orc.rse(x.astype(np.float64), orc.reconstruct_full(cores))
+    got = trg.rse(x, cores)
+    assert abs(got - want) <= (F64_TOL if dtype == np.float64 else F32_TOL) * want
+
+
+def test_rse_zero_reference_is_error(trg):
+    with pytest.raises(ValueError, match="zero norm"):
+        trg.rse(np.zeros((3, 4, 5)), orc.random_factors([3, 4, 5], [1, 1, 1], 0))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_synthesize_parity(trg, ctx, dtype):
+    dims, ranks = [30, 20, 10], [3, 2, 4]
+    cores = orc.random_factors(dims, ranks, 0)
+    want = orc.add_noise(orc.reconstruct_full(cores), 30.0, 1)
+    t = trg.DeviceTensor(ctx, dims, dtype).synthesize(cores, snr_db=30.0, noise_seed=1)
+    got = t.numpy()
+    assert relerr(got, want) < (1e-12 if dtype == np.float64 else 1e-6)
+
+
+# ---------------------------------------------------------------- Algorithm 1 end to end
+def test_rtrals_c1_parity(trg):
+    """C1 (BASELINE configs[0]) at full size: 100^3 f64, TR rank 5, 40 dB, K=10, 20 sweeps, seed 0."""
+    dims, R = [100, 100, 100], 5
+    x = orc.add_noise(orc.reconstruct_full(orc.random_factors(dims, [R] * 3, 0)), 40.0, 1)
+    want = orc.rtrd("als", x, [10] * 3, ranks=[R] * 3, max_sweeps=20, cfg_seed=0, spec_seed=0)
+    got = trg.rtrals(x, trg.SolverConfig(ranks=[R] * 3, max_sweeps=20, seed=0), trg.ProjectionSpec([10] * 3, 0))
+    assert got.sweeps_run == want.sweeps_run == 20
+    np.testing.assert_allclose(got.rse_history, want.rse_history, rtol=1e-8)
+    assert abs(got.rse_history[-1] - want.rse_history[-1]) <= 1e-8 * want.rse_history[-1]
+    # ALS trajectories are deterministic; cores agree up to rounding amplification
+    recon_g = orc.reconstruct_full(got.factors)
+    recon_w = orc.reconstruct_full(want.cores)
+    assert relerr(recon_g, recon_w) < 1e-8
+
+
+def test_rtrsvd_parity_with_sign_normalisation(trg):
+    dims = [30, 28, 26, 24]
+    x = orc.add_noise(orc.reconstruct_full(orc.random_factors(dims, [3] * 4, 0)), 30.0, 1)
+    K = [9, 9, 9, 9]
+    want = orc.rtrd("svd", x, K, tol=1e-3, cfg_seed=0, spec_seed=0)
+    got = trg.rtrsvd(x, trg.SolverConfig(tolerance=1e-3), trg.ProjectionSpec(K, 0))
+    assert got.ranks == want.ranks
+    assert abs(got.rse_history[-1] - want.rse_history[-1]) <= F64_TOL * want.rse_history[-1] + 1e-14
+    assert relerr(orc.reconstruct_full(got.factors), orc.reconstruct_full(want.cores)) < 1e-9
+
+
+def test_rtrals_identity_projection_matches_trals(trg):
+    # SPEC.md:296 / acceptance 4: K_n = I_n gives the plain solver, bit-identical path
+    x = tr_tensor([8, 7, 6], [2, 2, 2], 5, snr=30.0)
+    plain = orc.solve("als", x, ranks=[2, 2, 2], max_sweeps=6, seed=4)
+    got = trg.rtrals(x, trg.SolverConfig(ranks=[2, 2, 2], max_sweeps=6, seed=4), trg.ProjectionSpec([8, 7, 6], 1))
+    assert abs(got.rse_history[-1] - plain.rse_history[-1]) < 1e-8
+
+
+def test_rtrals_recovery_spec_297(trg):
+    x = tr_tensor([30, 30, 30], [3, 4, 3], 2)
+    got = trg.rtrals(x, trg.SolverConfig(ranks=[3, 4, 3], max_sweeps=50), trg.ProjectionSpec([15] * 3, 0))
+    assert got.rse_history[-1] < 1e-4
+
+
+def test_rtrals_f32_parity(trg):
+    dims = [64, 48, 40]
+    x = tr_tensor(dims, [4, 4, 4], 7, snr=40.0).astype(np.float32)
+    want = orc.rtrd("als", x.astype(np.float64), [16, 16, 16], ranks=[4] * 3, max_sweeps=5)
+    got = trg.rtrals(x, trg.SolverConfig(ranks=[4] * 3, max_sweeps=5), trg.ProjectionSpec([16] * 3, 0))
+    assert abs(got.rse_history[-1] - want.rse_history[-1]) <= F32_TOL * want.rse_history[-1]
+
+
+def test_decompose_device_resident_equals_host(trg, ctx):
+    x = tr_tensor([40, 30, 20], [3, 3, 3], 1, snr=30.0)
+    cfg, spec = trg.SolverConfig(ranks=[3, 3, 3], max_sweeps=4), trg.ProjectionSpec([9, 9, 9], 2)
+    a = trg.rtrals(x, cfg, spec)
+    b = trg.rtrals(trg.DeviceTensor.from_numpy(ctx, x), cfg, spec)
+    np.testing.assert_array_equal(a.rse_history, b.rse_history)
+    for ca, cb in zip(a.factors, b.factors):
+        np.testing.assert_array_equal(ca, cb)
+
+
+def test_launch_counter_and_profiling(trg, ctx):
+    x = trg.DeviceTensor.from_numpy(ctx, np.random.default_rng(0).standard_normal((20, 20, 20)))
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    sk = trg.DeviceSketch(ctx, x, trg.ProjectionSpec([4, 4, 4], 0))
+    sk.projected()
+    ctx.set_profiling(False)
+    labels = ctx.kernel_labels()
+    assert "sketch_m0" in labels and "ttm_m0" in labels and "qr" in labels
+    assert ctx.launch_count() >= 12  # 3 modes x (sketch + reduce + qr + ttm)
