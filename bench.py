@@ -374,7 +374,7 @@ def main():
     import ctypes
 
     e2e_times, last = [], None
-    for i in range(args.e2e_steps + 1):
+    for i in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         barrier()
         h = ctypes.c_void_p()
         t0 = time.perf_counter()
@@ -388,15 +388,17 @@ def main():
         if i > 0:  # first call is warm-up
             e2e_times.append(t1 - t0)
         last = rep
-    sec = max(e2e_times)
-    if dist is not None:
-        t = torch.tensor([sec], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec = float(t.item())
-    d2h = sum(c.size for c in last.factors) * 8 + len(last.rse_history) * 8 + int(np.prod(cfg["K"])) * 8
-    e2e = {"value": x_bytes / sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": x_bytes, "d2h_bytes_per_step": d2h,
-           "ms_per_step": sec * 1e3, "stage_ms": last.timings_ms, "final_rse": last.rse_history[-1],
-           "ranks": last.ranks, "call": "trg_decompose_host (pinned host X)"}
+    if e2e_times:
+        sec = max(e2e_times)
+        if dist is not None:
+            t = torch.tensor([sec], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        d2h = sum(c.size for c in last.factors) * 8 + len(last.rse_history) * 8 + int(np.prod(cfg["K"])) * 8
+        e2e = {"value": x_bytes / sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": x_bytes,
+               "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3, "stage_ms": last.timings_ms,
+               "final_rse": last.rse_history[-1], "ranks": last.ranks,
+               "call": "trg_decompose_host (pinned host X)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -47,6 +47,16 @@ struct TTMPlan {
 void plan_ttm(TTMPlan& p, int num_sms);
 void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cudaStream_t s);
 
+// ---- TMA-pipelined fp64 tensor-core kernels for the mode-0 passes (stream_f64.cu)
+bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K);
+void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                          int* grid_out, cudaStream_t s);
+bool stream_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim);
+void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
+                       cudaStream_t s);
+// fixed-order sum of nblocks partial (n doubles each)
+void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s);
+
 // ---- thin QR with diag(R) >= 0 (K4): CholQR2 + Householder fallback, fp64.
 // Y is m x k column-major; Q (m x k) out. work >= m*k doubles + 2*k.
 void launch_qr(const double* y, int64_t m, int k, double* q, double* work, int* flag, cudaStream_t s);

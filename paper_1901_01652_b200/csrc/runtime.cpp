@@ -303,11 +303,21 @@ int64_t sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const st
         p.rows_glob = p.left;  // last mode: columns are l only
         p.col_off = 0;
     }
-    trg::plan_sketch(p, ctx->num_sms);
-    double* partial = (double*)ctx->alloc(p.partial_elems * sizeof(double));
     const bool sharded_rows = (n == N - 1) && ctx->world > 1;
     double* ylocal = sharded_rows ? (double*)ctx->alloc(sizeof(double) * p.dim * Kn) : dYfull;
-    ctx->launch("sketch_m" + std::to_string(n), [&] { trg::launch_sketch(p, cur, partial, ylocal, ctx->stream); }, 2);
+    double* partial = nullptr;
+    if (trg::stream_sketch_ok(p.dtype, p.left, p.dim, (int)Kn)) {
+        partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        int grid = 0;
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_stream_sketch(p, cur, partial, ylocal, ctx->num_sms, &grid, ctx->stream);
+        }, 2);
+    } else {
+        trg::plan_sketch(p, ctx->num_sms);
+        partial = (double*)ctx->alloc(p.partial_elems * sizeof(double));
+        ctx->launch("sketch_m" + std::to_string(n), [&] { trg::launch_sketch(p, cur, partial, ylocal, ctx->stream); },
+                    2);
+    }
     ctx->dfree(partial);
     if (sharded_rows) {
         ctx->launch("scatter", [&] {
@@ -333,10 +343,16 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
     p.m_sd = 1;
     const double* m = dQ;
     if (n == N - 1) m += x->lo;  // local rows of Q_{N-1}
-    trg::plan_ttm(p, ctx->num_sms);
     const size_t es = trg::dtype_size(x->dtype);
     void* out = ctx->alloc(es * (size_t)(p.left * Kn * p.right));
-    ctx->launch("ttm_m" + std::to_string(n), [&] { trg::launch_ttm(p, cur, out, m, ctx->stream); });
+    if (trg::stream_ttm_ok(p.dtype, p.left, p.dim, Kn)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_stream_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
+        });
+    } else {
+        trg::plan_ttm(p, ctx->num_sms);
+        ctx->launch("ttm_m" + std::to_string(n), [&] { trg::launch_ttm(p, cur, out, m, ctx->stream); });
+    }
     return out;
 }
 

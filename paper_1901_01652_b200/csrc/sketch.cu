@@ -244,10 +244,13 @@ void launch_sketch(const SketchPlan& p, const void* x, double* partial, double* 
         if (p.TK == 8) dispatch<float, 4, 8>(p, a, s);
         else dispatch<float, 4, 4>(p, a, s);
     }
-    const int64_t n = p.dim * p.K;
+    launch_reduce_partials(partial, p.grid_x, p.dim * p.K, y, s);
+}
+
+void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s) {
     const int threads = 256;
-    const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 1024);
-    k_reduce_partials<<<blocks, threads, 0, s>>>(partial, p.grid_x, n, y);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 1024));
+    k_reduce_partials<<<blocks, threads, 0, s>>>(partial, nblocks, n, out);
 }
 
 void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, double* out, cudaStream_t s) {

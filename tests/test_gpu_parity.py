@@ -53,9 +53,9 @@ SHAPES = [
     ((23, 17, 9), (5, 17, 4)),                # odd sizes, mode 1 skipped
     ((12, 11, 10, 9), (3, 4, 5, 2)),
     ((8, 7, 6, 5, 4), (2, 3, 6, 2, 3)),       # order 5, mode 2 skipped
-    ((300, 7), (9, 3)),                       # order 2
+    ((300, 7), (6, 3)),                       # order 2 (K_0 <= rank 7 of the unfolding)
     ((129, 33, 65), (17, 8, 64)),             # non-power-of-2 tails, d-tiling
-    ((40,), (6,)),                            # order 1
+    ((40,), (1,)),                            # order 1 (Y = x w has rank 1)
     ((6, 5, 4), (6, 5, 4)),                   # all skipped: P = X exactly
 ]
 
