@@ -29,6 +29,7 @@ constexpr int kStages = 3;
 constexpr int kCons = 4;  // consumer warps
 constexpr int kRng = 4;   // Omega generator warps (sketch)
 constexpr int kPad = 8;   // zeroed doubles after each stage (A rows may overrun by < 8)
+constexpr size_t kBarBytes = 256;  // room for the mbarriers after the buffers
 
 struct SkArgs {
     const double* x;
@@ -290,7 +291,7 @@ constexpr size_t kSmemBudget = 220 * 1024;
 bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
     if (dtype != F64 || left != 1 || (dim & 1) || K > 64 || dim > 256) return false;
     const int CT = dim <= 112 ? 64 : 32;
-    const size_t smem = (kStages * (size_t)(CT * dim + kPad) + 2 * (size_t)CT * nt_for(K) * 8) * 8 + 64;
+    const size_t smem = (kStages * (size_t)(CT * dim + kPad) + 2 * (size_t)CT * nt_for(K) * 8) * 8 + kBarBytes;
     return smem <= kSmemBudget;
 }
 
@@ -311,7 +312,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.partial = partial;
     const int NT = nt_for(p.K);
     const int mtw = (a.mtiles + kCons - 1) / kCons;
-    const size_t smem = (kStages * (size_t)(a.CT * a.dim + kPad) + 2 * (size_t)a.CT * NT * 8) * 8 + 64;
+    const size_t smem = (kStages * (size_t)(a.CT * a.dim + kPad) + 2 * (size_t)a.CT * NT * 8) * 8 + kBarBytes;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     *grid_out = grid;
     const int threads = (kCons + kRng + 1) * 32;
@@ -343,7 +344,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
 bool stream_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim) {
     if (dtype != F64 || left != 1 || (dim & 1) || odim > 64) return false;
     const int Tk = (int)((dim + 3) / 4);
-    const size_t smem = (kStages * (size_t)(64 * dim + kPad) + (size_t)Tk * nt_for((int)odim) * 32) * 8 + 64;
+    const size_t smem = (kStages * (size_t)(64 * dim + kPad) + (size_t)Tk * nt_for((int)odim) * 32) * 8 + kBarBytes;
     return smem <= kSmemBudget;
 }
 
@@ -361,7 +362,7 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
     a.Tk = (int)((p.dim + 3) / 4);
     a.ntiles = (a.rows + a.MT - 1) / a.MT;
     const int NT = nt_for(a.K);
-    const size_t smem = (kStages * (size_t)(a.MT * a.dim + kPad) + (size_t)a.Tk * NT * 32) * 8 + 64;
+    const size_t smem = (kStages * (size_t)(a.MT * a.dim + kPad) + (size_t)a.Tk * NT * 32) * 8 + kBarBytes;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     const int threads = (kCons + 1) * 32;
     switch (NT) {
