@@ -54,6 +54,13 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
 bool stream_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim);
 void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                        cudaStream_t s);
+// ---- cp.async-gathered fp64 tensor-core kernels for modes with left > 1 (slab_f64.cu)
+bool slab_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
+void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                        cudaStream_t s);
+bool slab_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim, int64_t ncols);
+void launch_slab_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
+                     cudaStream_t s);
 // fixed-order sum of nblocks partial (n doubles each)
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s);
 

@@ -312,6 +312,11 @@ int64_t sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const st
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_stream_sketch(p, cur, partial, ylocal, ctx->num_sms, &grid, ctx->stream);
         }, 2);
+    } else if (trg::slab_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.left * p.right)) {
+        partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_slab_sketch(p, cur, partial, ylocal, ctx->num_sms, ctx->stream);
+        }, 2);
     } else {
         trg::plan_sketch(p, ctx->num_sms);
         partial = (double*)ctx->alloc(p.partial_elems * sizeof(double));
@@ -348,6 +353,10 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
     if (trg::stream_ttm_ok(p.dtype, p.left, p.dim, Kn)) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
+        });
+    } else if (trg::slab_ttm_ok(p.dtype, p.left, p.dim, Kn, p.left * p.right)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_slab_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
         });
     } else {
         trg::plan_ttm(p, ctx->num_sms);

@@ -149,11 +149,26 @@ __global__ void __launch_bounds__(256) k_sketch(SketchArgs a) {
     }
 }
 
-__global__ void k_reduce_partials(const double* __restrict__ partial, int nblocks, int64_t n, double* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nblocks; ++b) s += partial[(int64_t)b * n + i];
-        out[i] = s;
+// out[i] = sum_b partial[b][i]: a CTA owns 32 consecutive outputs (one per lane),
+// its 8 warps stride over the partials (b = w, w + 8, ...), and the 8 warp sums
+// are combined in warp order — a fixed summation tree, so the result does not
+// depend on scheduling.
+__global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ partial, int nblocks, int64_t n,
+                                                         double* __restrict__ out) {
+    __shared__ double red[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (i < n) {
+#pragma unroll 4
+        for (int b = warp; b < nblocks; b += 8) s += partial[(int64_t)b * n + i];
+    }
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && i < n) {
+        double t = red[0][lane];
+        for (int w = 1; w < 8; ++w) t += red[w][lane];
+        out[i] = t;
     }
 }
 
@@ -248,9 +263,8 @@ void launch_sketch(const SketchPlan& p, const void* x, double* partial, double* 
 }
 
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s) {
-    const int threads = 256;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 1024));
-    k_reduce_partials<<<blocks, threads, 0, s>>>(partial, nblocks, n, out);
+    const int blocks = (int)std::max<int64_t>(1, (n + 31) / 32);
+    k_reduce_partials<<<blocks, 256, 0, s>>>(partial, nblocks, n, out);
 }
 
 void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, double* out, cudaStream_t s) {

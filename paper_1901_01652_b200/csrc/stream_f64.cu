@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kStages = 3;
 constexpr int kCons = 4;  // consumer warps
-constexpr int kRng = 4;   // Omega generator warps (sketch)
+constexpr int kRng = 8;   // Omega generator warps (sketch)
 constexpr int kPad = 8;   // zeroed doubles after each stage (A rows may overrun by < 8)
 constexpr size_t kBarBytes = 256;  // room for the mbarriers after the buffers
 
@@ -123,6 +123,8 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
         return;
     }
     // ---------------- consumer warps: Y(d, k) += sum_c X(d, c) Omega(c, k)
+    // Warp w takes k-steps t = w, w + kCons, ... of every tile with full-height
+    // accumulators, so the work is balanced whatever dim is.
     double acc[MTW][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MTW; ++mt)
@@ -134,19 +136,17 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
         const int b = j & 1;
         mbar_wait(&full_x[s], (j / kStages) & 1);
         mbar_wait(&full_o[b], (j >> 1) & 1);
-        const double* X = stages + s * stage_elems;
+        const double* X = stages + s * stage_elems + r * dim + q;
         const double* O = omega + b * omega_elems;
-#pragma unroll 2
-        for (int t = 0; t < CT / 4; ++t) {
+        for (int t = warp; t < CT / 4; t += kCons) {
             double bv[NT];
 #pragma unroll
             for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
-            const double* xrow = X + (4 * t + r) * dim + q;
+            const double* xrow = X + 4 * t * dim;
 #pragma unroll
             for (int mt = 0; mt < MTW; ++mt) {
-                const int m = warp + kCons * mt;
-                if (m < a.mtiles) {
-                    const double av = xrow[8 * m];
+                if (mt < a.mtiles) {
+                    const double av = xrow[8 * mt];
 #pragma unroll
                     for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av, bv[jn]);
                 }
@@ -155,18 +155,28 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
         mbar_arrive(&empty_x[s]);
         mbar_arrive(&empty_o[b]);
     }
-    double* out = a.partial + (int64_t)blockIdx.x * dim * a.K;
+    // fixed-order reduction of the consumer warps through (consumed) stage 0
+    asm volatile("bar.sync 1, %0;" ::"n"(kCons * 32));
+    double* red = stages;
+    const int ld = 8 * MTW;
+    for (int w = 0; w < kCons; ++w) {
+        if (warp == w) {
 #pragma unroll
-    for (int mt = 0; mt < MTW; ++mt) {
-        const int m = warp + kCons * mt;
-        const int64_t d = 8 * m + q;
-        if (m >= a.mtiles || d >= dim) continue;
+            for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
-        for (int jn = 0; jn < NT; ++jn) {
-            const int k = 8 * jn + 2 * r;
-            if (k < a.K) out[d + dim * k] = acc[mt][jn][0];
-            if (k + 1 < a.K) out[d + dim * (k + 1)] = acc[mt][jn][1];
+                for (int jn = 0; jn < NT; ++jn) {
+                    double* p0 = red + (8 * mt + q) + ld * (8 * jn + 2 * r);
+                    *p0 = (w == 0 ? 0.0 : *p0) + acc[mt][jn][0];
+                    p0[ld] = (w == 0 ? 0.0 : p0[ld]) + acc[mt][jn][1];
+                }
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(kCons * 32));
+    }
+    double* out = a.partial + (int64_t)blockIdx.x * dim * a.K;
+    for (int e = tid; e < dim * a.K; e += kCons * 32) {
+        const int k = e / (int)dim;
+        const int d = e - k * (int)dim;
+        out[d + dim * k] = red[d + ld * k];
     }
 }
 
@@ -289,7 +299,7 @@ constexpr size_t kSmemBudget = 220 * 1024;
 
 // ---------------------------------------------------------------- sketch
 bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
-    if (dtype != F64 || left != 1 || (dim & 1) || K > 64 || dim > 256) return false;
+    if (dtype != F64 || left != 1 || (dim & 1) || K > 64 || dim > 128) return false;
     const int CT = dim <= 112 ? 64 : 32;
     const size_t smem = (kStages * (size_t)(CT * dim + kPad) + 2 * (size_t)CT * nt_for(K) * 8) * 8 + kBarBytes;
     return smem <= kSmemBudget;
@@ -311,7 +321,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.D = p.D;
     a.partial = partial;
     const int NT = nt_for(p.K);
-    const int mtw = (a.mtiles + kCons - 1) / kCons;
+    const int mtw = a.mtiles;  // full-height accumulators per consumer warp
     const size_t smem = (kStages * (size_t)(a.CT * a.dim + kPad) + 2 * (size_t)a.CT * NT * 8) * 8 + kBarBytes;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     *grid_out = grid;
@@ -328,12 +338,14 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
         case 4: TRG_SK(MTW, 4); break;   \
         default: TRG_SK(MTW, 8); break;  \
     }
-    if (mtw <= 2) {
-        TRG_SK_NT(2)
-    } else if (mtw <= 4) {
+    if (mtw <= 4) {
         TRG_SK_NT(4)
-    } else {
+    } else if (mtw <= 8) {
         TRG_SK_NT(8)
+    } else if (mtw <= 13) {
+        TRG_SK_NT(13)
+    } else {
+        TRG_SK_NT(16)
     }
 #undef TRG_SK_NT
 #undef TRG_SK
