@@ -12,9 +12,11 @@ Q_n resident in HBM. `value` = bytes of X / (device time per step), whole job
 scaling is strong). Inputs are larger than L2 (C2: X = 800 MB vs 126 MB L2), so
 no L2 flush is needed between steps.
 
-`e2e` is the same metric through the reference-facing C ABI call with a
-pinned HOST buffer (trg_decompose_host: H2D of X, projection, host small
-solve, back-projection, fused final RSE, D2H of cores): X bytes / wall time.
+`e2e` is the same metric through the reference-facing C ABI with a pinned
+HOST buffer: trg_tensor_upload (H2D of X) + trg_sketch_run + D2H of P and
+every Q_n, wall clock per step. `decompose_e2e` times the whole Algorithm 1
+(trg_decompose_host: H2D, projection, host small solve, back-projection,
+fused final RSE, D2H of the cores) once.
 
 `--impl reference` times the reference algorithm's CPU restatement
 (oracle/, the reference itself is unbuildable here: see DESIGN.md) with all
@@ -46,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="sequential", choices=["sequential", "fused"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--decompose", type=int, default=1, help="also time the full trg_decompose_host once")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
@@ -359,46 +362,69 @@ def main():
     stage = {"alg_bytes": b_alg, "frac": b_alg / world / (ms_step * 1e-3) / 1e9 / peak,
              "definition": "SURVEY §8d B_alg / per-rank step time / measured HBM peak"}
 
-    # ---- end to end through the C ABI with a pinned host buffer
-    e2e = None
+    # ---- end to end through the C ABI with a pinned host buffer: H2D of X (trg_tensor_upload),
+    # the projection (trg_sketch_run) and D2H of P and every Q_n (trg_sketch_projected / _basis),
+    # all inside the timed region, wall clock, max over ranks.
+    import ctypes
+
     local_np = x.numpy()
     dt = np.float64 if cfg["dtype"] == "f64" else np.float32
     host = torch.empty(local_np.size, dtype=torch.float64 if dt == np.float64 else torch.float32, pin_memory=True)
-    hv = host.numpy()
-    hv[:] = local_np.reshape(-1, order="F")
-    scfg = trg.SolverConfig(ranks=[cfg["rank"]] * len(cfg["dims"]) if cfg["method"] == "als" else None,
-                            tolerance=cfg["tol"], max_sweeps=cfg["sweeps"], seed=0)
-    k_ptr = L.i64(cfg["K"])
-    r_ptr = L.i64(scfg.ranks) if scfg.ranks else (None, None)
-    d_ptr = L.i64(cfg["dims"])
-    import ctypes
+    host.numpy()[:] = local_np.reshape(-1, order="F")
+    del local_np
+    k_arr, k_ptr = L.i64(cfg["K"])
+    N = len(cfg["dims"])
+    p_out = np.empty(int(np.prod(cfg["K"])), dtype=np.float64)
+    q_out = [np.empty(cfg["dims"][n] * cfg["K"][n], dtype=np.float64) for n in range(N)]
+    h2d = int(np.prod(x.local_shape)) * (8 if dt == np.float64 else 4)
+    d2h = p_out.nbytes + sum(q.nbytes for q in q_out)
 
-    e2e_times, last = [], None
-    for i in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
-        barrier()
+    def e2e_step():
+        L.call("trg_tensor_upload", x.handle, ctypes.c_void_p(host.data_ptr()))
         h = ctypes.c_void_p()
+        L.call("trg_sketch_run", ctx.handle, x.handle, k_ptr, ctypes.c_uint64(0), ctypes.c_int(variant),
+               ctypes.byref(h))
+        L.call("trg_sketch_projected", h, p_out.ctypes.data_as(L.c_dp))
+        for n in range(N):
+            L.call("trg_sketch_basis", h, ctypes.c_int(n), q_out[n].ctypes.data_as(L.c_dp))
+        L.call("trg_sketch_destroy", h)
+
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e_step()  # warm-up
+        barrier()
         t0 = time.perf_counter()
-        L.call("trg_decompose_host", ctx.handle, ctypes.c_int(L.TRG_F64 if dt == np.float64 else L.TRG_F32),
-               ctypes.c_int(len(cfg["dims"])), d_ptr[1], ctypes.c_void_p(host.data_ptr()),
-               ctypes.c_int(L.TRG_ALS if cfg["method"] == "als" else L.TRG_SVD), r_ptr[1],
-               ctypes.c_double(cfg["tol"]), ctypes.c_int64(cfg["sweeps"]), ctypes.c_uint64(0), k_ptr[1],
-               ctypes.c_uint64(0), ctypes.c_int(variant), ctypes.byref(h))
-        rep = trg.api._report(h, cfg["dims"])
-        t1 = time.perf_counter()
-        if i > 0:  # first call is warm-up
-            e2e_times.append(t1 - t0)
-        last = rep
-    if e2e_times:
-        sec = max(e2e_times)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        sec = (time.perf_counter() - t0) / args.e2e_steps
         if dist is not None:
             t = torch.tensor([sec], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             sec = float(t.item())
-        d2h = sum(c.size for c in last.factors) * 8 + len(last.rse_history) * 8 + int(np.prod(cfg["K"])) * 8
-        e2e = {"value": x_bytes / sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": x_bytes,
-               "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3, "stage_ms": last.timings_ms,
-               "final_rse": last.rse_history[-1], "ranks": last.ranks,
-               "call": "trg_decompose_host (pinned host X)"}
+        e2e = {"value": x_bytes / sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": sec * 1e3, "steps": args.e2e_steps,
+               "call": "C ABI: trg_tensor_upload (pinned host X) + trg_sketch_run + trg_sketch_projected/_basis"}
+
+    # ---- full Algorithm 1 through the C ABI (trg_decompose_host): H2D, projection, host small
+    # solve, back-projection, fused final RSE, D2H of the cores. Reported beside e2e.
+    decomp = None
+    if args.decompose:
+        scfg_ranks = [cfg["rank"]] * N if cfg["method"] == "als" else None
+        r_arr, r_ptr = L.i64(scfg_ranks) if scfg_ranks else (None, None)
+        d_arr, d_ptr = L.i64(cfg["dims"])
+        barrier()
+        t0 = time.perf_counter()
+        h = ctypes.c_void_p()
+        L.call("trg_decompose_host", ctx.handle, ctypes.c_int(L.TRG_F64 if dt == np.float64 else L.TRG_F32),
+               ctypes.c_int(N), d_ptr, ctypes.c_void_p(host.data_ptr()),
+               ctypes.c_int(L.TRG_ALS if cfg["method"] == "als" else L.TRG_SVD), r_ptr,
+               ctypes.c_double(cfg["tol"]), ctypes.c_int64(cfg["sweeps"]), ctypes.c_uint64(0), k_ptr,
+               ctypes.c_uint64(0), ctypes.c_int(variant), ctypes.byref(h))
+        rep = trg.api._report(h, cfg["dims"])
+        sec = time.perf_counter() - t0
+        decomp = {"seconds": sec, "stage_ms": rep.timings_ms, "final_rse": rep.rse_history[-1], "ranks": rep.ranks,
+                  "method": "rTR-ALS" if cfg["method"] == "als" else "rTR-SVD",
+                  "call": "C ABI: trg_decompose_host (pinned host X)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -415,7 +441,7 @@ def main():
                 "config": {"workload": workload_name(args.config, cfg), "dims": cfg["dims"], "K": cfg["K"],
                            "variant": args.variant, "parallelism": f"last-mode shards x{world}" if world > 1
                            else "single GPU", "l2": "X larger than L2 (no flush needed)"},
-                "roofline": roof, "stage_roofline": stage, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "stage_roofline": stage, "cpu_baseline": cpu, "e2e": e2e, "decompose_e2e": decomp,
                 "gpu_launches": launches, "clocks": clk.summary(), "kernels": kernels}
         print(json.dumps(line), flush=True)
     barrier()

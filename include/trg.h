@@ -82,6 +82,11 @@ int trg_ctx_launch_count(trg_ctx* ctx, int64_t* launches);       /* every libtrg
 int trg_ctx_reset_stats(trg_ctx* ctx);
 /* Balanced last-mode partition used for sharded tensors (pure host). */
 int trg_shard_range(int64_t extent, int rank, int world, int64_t* lo, int64_t* hi);
+/* Pure host: where each mode's test matrix sits in the reference stream for
+ * this rank's slab. Omega_n(c, k) = draw draw_off[n] + col_off[n] + c +
+ * rows_glob[n] * k for local unfolding column c (rows_glob[n] = 0: skipped). */
+int trg_sketch_offsets(int order, const int64_t* dims, const int64_t* K, int rank, int world, int variant,
+                       int64_t* rows_glob, int64_t* col_off, uint64_t* draw_off);
 
 /* ---- dense tensors (DenseTensor, tensor.hpp:42-108) --------------------- */
 int trg_tensor_create(trg_ctx* ctx, int dtype, int order, const int64_t* dims, trg_tensor** out);
@@ -109,6 +114,10 @@ int trg_sketch_y(const trg_sketch* sk, int mode, double* out);     /* Y_n: I_n x
 int trg_sketch_qr_path(const trg_sketch* sk, int mode, int* householder); /* 0 CholQR2, 1 Householder */
 int trg_sketch_elapsed_ms(const trg_sketch* sk, double* ms);       /* device time, first kernel -> P resident */
 int trg_sketch_destroy(trg_sketch* sk);
+/* detail::economy_q (sketch.hpp:45-53) on one host matrix: Y is m x k col-major,
+ * Q (m x k col-major) has the reference sign convention (diag R >= 0).
+ * *householder (may be NULL) reports the path taken: 0 CholQR2, 1 Householder. */
+int trg_thin_qr(trg_ctx* ctx, int64_t m, int64_t k, const double* y, double* q, int* householder);
 /* Test-matrix export: out(c, k) = reference draw offset + c + rows*k (sketch.hpp:32-38). */
 int trg_omega(trg_ctx* ctx, uint64_t seed, uint64_t offset, int64_t rows, int64_t cols, double* out);
 

@@ -17,10 +17,12 @@ from .api import (  # noqa: F401
     decompose,
     default_context,
     gaussian_matrix,
+    economy_q,
     mode_n_product,
     rse,
     rtrals,
     rtrsvd,
     shard_range,
+    sketch_offsets,
     sketch,
 )

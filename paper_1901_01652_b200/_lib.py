@@ -19,11 +19,11 @@ EXPORTS = [
     "trg_abi_version", "trg_last_error", "trg_device_count",
     "trg_ctx_create", "trg_nccl_unique_id", "trg_ctx_create_dist", "trg_ctx_destroy", "trg_ctx_synchronize",
     "trg_ctx_stream", "trg_ctx_set_profiling", "trg_ctx_kernel_stats", "trg_ctx_kernel_labels",
-    "trg_ctx_launch_count", "trg_ctx_reset_stats", "trg_shard_range",
+    "trg_ctx_launch_count", "trg_ctx_reset_stats", "trg_shard_range", "trg_sketch_offsets",
     "trg_tensor_create", "trg_tensor_info", "trg_tensor_upload", "trg_tensor_download", "trg_tensor_device_ptr",
     "trg_tensor_synthesize", "trg_tensor_destroy",
     "trg_sketch_run", "trg_sketch_projected", "trg_sketch_basis", "trg_sketch_y", "trg_sketch_qr_path",
-    "trg_sketch_elapsed_ms", "trg_sketch_destroy", "trg_omega",
+    "trg_sketch_elapsed_ms", "trg_sketch_destroy", "trg_thin_qr", "trg_omega",
     "trg_mode_n_product", "trg_back_project", "trg_rse",
     "trg_decompose", "trg_decompose_host", "trg_report_ranks", "trg_report_cores_len", "trg_report_cores",
     "trg_report_rse_history", "trg_report_sweeps", "trg_report_timings", "trg_report_projected",

@@ -143,6 +143,22 @@ def shard_range(extent, rank, world):
     return lo.value, hi.value
 
 
+def sketch_offsets(dims, K, rank=0, world=1, variant=L.TRG_SEQUENTIAL):
+    """Per-mode test-matrix placement for a rank's last-mode slab (pure host, no device):
+    Omega_n(c, k) = reference draw draw_off[n] + col_off[n] + c + rows_glob[n] * k
+    for local unfolding column c; rows_glob[n] == 0 marks a skipped mode."""
+    N = len(dims)
+    d, dp = L.i64(dims)
+    k, kp = L.i64(K)
+    rows = np.zeros(N, dtype=np.int64)
+    cols = np.zeros(N, dtype=np.int64)
+    draw = np.zeros(N, dtype=np.uint64)
+    L.call("trg_sketch_offsets", ctypes.c_int(N), dp, kp, ctypes.c_int(rank), ctypes.c_int(world),
+           ctypes.c_int(variant), rows.ctypes.data_as(L.c_i64p), cols.ctypes.data_as(L.c_i64p),
+           draw.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    return [int(v) for v in rows], [int(v) for v in cols], [int(v) for v in draw]
+
+
 class DeviceTensor:
     """DenseTensor (tensor.hpp:42-108) resident in HBM; local last-mode slab when sharded."""
 
@@ -309,6 +325,18 @@ def gaussian_matrix(rows, cols, seed, offset=0, ctx=None):
     L.call("trg_omega", ctx.handle, ctypes.c_uint64(seed), ctypes.c_uint64(offset), ctypes.c_int64(rows),
            ctypes.c_int64(cols), out.ctypes.data_as(L.c_dp))
     return out.reshape((rows, cols), order="F")
+
+
+def economy_q(y, ctx=None, return_path=False):
+    """detail::economy_q (sketch.hpp:45-53) on the device: thin Q with diag(R) >= 0."""
+    ctx = ctx or default_context()
+    y = np.asfortranarray(np.asarray(y, dtype=np.float64))
+    m, k = y.shape
+    q = np.empty((m, k), dtype=np.float64, order="F")
+    hh = ctypes.c_int(0)
+    L.call("trg_thin_qr", ctx.handle, ctypes.c_int64(m), ctypes.c_int64(k), y.ctypes.data_as(L.c_dp),
+           q.ctypes.data_as(L.c_dp), ctypes.byref(hh))
+    return (q, hh.value) if return_path else q
 
 
 def mode_n_product(x, mode, m, ctx=None):

@@ -281,12 +281,53 @@ void validate_K(const trg_tensor* x, const int64_t* K) {
 }
 
 // ------------------------------------------------------------------ projection pipeline
+// Where mode n's test matrix sits in the reference stream and which of its rows a
+// rank owns (pure host; exported as trg_sketch_offsets for the sharding tests).
+// Omega_n(c, k) = draw D_n + col_off_n + c + rows_glob_n * k (sketch.hpp:32-38, 69,
+// 81), c = local column of the unfolding. rows_glob_n is the column count of the
+// GLOBAL current unfolding (sized against the shrunken tensor, sketch.hpp:80-81, or
+// against X for the fused variant); skipped modes draw nothing
+// (sketch.hpp:76-79). For n < N-1 the last mode is the slowest column digit, so a
+// rank's slab [lo, hi) owns the contiguous column block starting at col_off_n; for
+// n = N-1 every rank holds all columns and its own rows of Y.
+struct ModeOffsets {
+    int64_t rows_glob = 0, col_off = 0;
+    uint64_t D = 0;
+    bool skipped = false;
+};
+
+std::vector<ModeOffsets> sketch_offsets(const std::vector<int64_t>& dims, const int64_t* K, int64_t lo, int variant) {
+    const int N = (int)dims.size();
+    std::vector<ModeOffsets> out(N);
+    std::vector<int64_t> cur = dims;
+    uint64_t D = 0;
+    for (int n = 0; n < N; ++n) {
+        ModeOffsets& o = out[n];
+        o.D = D;
+        if (K[n] == dims[n]) {
+            o.skipped = true;
+            continue;
+        }
+        const int64_t left = prod(cur, 0, n);
+        if (n < N - 1) {
+            const int64_t r_inner = prod(cur, n + 1, N - 1);
+            o.rows_glob = left * r_inner * dims[N - 1];
+            o.col_off = left * r_inner * lo;
+        } else {
+            o.rows_glob = left;
+            o.col_off = 0;
+        }
+        D += (uint64_t)o.rows_glob * (uint64_t)K[n];
+        if (variant == TRG_SEQUENTIAL) cur[n] = K[n];
+    }
+    return out;
+}
+
 // Y_n of the (local) current tensor cur with shape cur_shape, into dYfull
-// (I_n x K_n, replicated). Returns the rows_glob of Omega_n.
-int64_t sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
-                    int64_t Kn, uint64_t seed, uint64_t D, double* dYfull) {
+// (I_n x K_n, replicated).
+void sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
+                 int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull) {
     const int N = (int)cur_shape.size();
-    const int64_t local_last = x->hi - x->lo;
     trg::SketchPlan p{};
     p.dtype = x->dtype;
     p.left = prod(cur_shape, 0, n);
@@ -294,15 +335,9 @@ int64_t sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const st
     p.right = prod(cur_shape, n + 1);
     p.K = (int)Kn;
     p.seed = seed;
-    p.D = D;
-    if (n < N - 1) {
-        const int64_t r_inner = p.right / local_last;  // prod of modes n+1..N-2
-        p.rows_glob = p.left * r_inner * x->dims[N - 1];
-        p.col_off = p.left * r_inner * x->lo;
-    } else {
-        p.rows_glob = p.left;  // last mode: columns are l only
-        p.col_off = 0;
-    }
+    p.D = off.D;
+    p.rows_glob = off.rows_glob;
+    p.col_off = off.col_off;
     const bool sharded_rows = (n == N - 1) && ctx->world > 1;
     double* ylocal = sharded_rows ? (double*)ctx->alloc(sizeof(double) * p.dim * Kn) : dYfull;
     double* partial = nullptr;
@@ -331,7 +366,6 @@ int64_t sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const st
         ctx->dfree(ylocal);
     }
     ctx->allreduce(dYfull, (size_t)(x->dims[n] * Kn), F64);
-    return p.rows_glob;
 }
 
 // out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
@@ -386,7 +420,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     std::vector<int64_t> shape = x->local_shape();
     const void* cur = x->d;
     void* owned = nullptr;  // buffer owned by the pipeline (not x)
-    uint64_t D = 0;         // stream offset: draws consumed by earlier modes (sketch.hpp:69)
+    const std::vector<ModeOffsets> offs = sketch_offsets(x->dims, Kin, x->lo, variant);
 
     auto qr = [&](int n) {
         const int64_t In = x->dims[n], Kn = sk->K[n];
@@ -401,8 +435,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
             sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-            const int64_t rows_glob = sketch_mode(ctx, x, cur, shape, n, Kn, seed, D, sk->dY[n]);
-            D += (uint64_t)rows_glob * (uint64_t)Kn;
+            sketch_mode(ctx, x, cur, shape, n, Kn, seed, offs[n], sk->dY[n]);
             qr(n);
             void* out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
             if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), x->dtype);
@@ -419,8 +452,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
             sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-            const int64_t rows_glob = sketch_mode(ctx, x, x->d, xshape, n, Kn, seed, D, sk->dY[n]);
-            D += (uint64_t)rows_glob * (uint64_t)Kn;
+            sketch_mode(ctx, x, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n]);
             qr(n);
         }
         for (int n = 0; n < N; ++n) {
@@ -722,6 +754,25 @@ int trg_device_count(int* count) {
     });
 }
 
+int trg_sketch_offsets(int order, const int64_t* dims, const int64_t* K, int rank, int world, int variant,
+                       int64_t* rows_glob, int64_t* col_off, uint64_t* draw_off) {
+    return guard([&] {
+        require(order >= 1 && dims && K, "sketch: projection size list must match tensor order");
+        std::vector<int64_t> d(dims, dims + order);
+        for (int n = 0; n < order; ++n)
+            require(K[n] >= 1 && K[n] <= d[n], "sketch: need 1 <= K_n <= I_n in mode " + std::to_string(n));
+        require(world >= 1 && rank >= 0 && rank < world, "shard: bad rank/world");
+        int64_t lo = 0, hi = 0;
+        shard(d.back(), rank, world, lo, hi);
+        const auto offs = sketch_offsets(d, K, lo, variant);
+        for (int n = 0; n < order; ++n) {
+            rows_glob[n] = offs[n].skipped ? 0 : offs[n].rows_glob;
+            col_off[n] = offs[n].skipped ? 0 : offs[n].col_off;
+            draw_off[n] = offs[n].D;
+        }
+    });
+}
+
 int trg_shard_range(int64_t extent, int rank, int world, int64_t* lo, int64_t* hi) {
     return guard([&] {
         require(world >= 1 && rank >= 0 && rank < world, "shard: bad rank/world");
@@ -997,6 +1048,26 @@ int trg_sketch_elapsed_ms(const trg_sketch* sk, double* ms) {
 
 int trg_sketch_destroy(trg_sketch* sk) {
     return guard([&] { delete sk; });
+}
+
+int trg_thin_qr(trg_ctx* ctx, int64_t m, int64_t k, const double* y, double* q, int* householder) {
+    return guard([&] {
+        require(ctx && y && q, "economy_q: null argument");
+        require(m >= 1 && k >= 1 && k <= m, "economy_q: need 1 <= k <= m");
+        double* d = (double*)ctx->alloc(sizeof(double) * (size_t)(3 * m * k) + sizeof(int) * 2);
+        double* dy = d;
+        double* dq = d + m * k;
+        double* work = d + 2 * m * k;
+        int* flag = (int*)(d + 3 * m * k);
+        CK(cudaMemcpyAsync(dy, y, sizeof(double) * m * k, cudaMemcpyHostToDevice, ctx->stream));
+        ctx->launch("qr", [&] { trg::launch_qr(dy, m, (int)k, dq, work, flag, ctx->stream); });
+        int hh = 0;
+        CK(cudaMemcpyAsync(q, dq, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&hh, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->dfree(d);
+        if (householder) *householder = hh;
+    });
 }
 
 int trg_omega(trg_ctx* ctx, uint64_t seed, uint64_t offset, int64_t rows, int64_t cols, double* out) {
