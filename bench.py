@@ -84,7 +84,10 @@ def alg_bytes(cfg, variant="sequential"):
 
 def kernel_bytes(cfg, label):
     """Algorithmic bytes of one launch of a labelled kernel (reads of its input tensor
-    + writes of its output tensor)."""
+    + writes of its output tensor). A fused "ttm_mN+sketch_mM" launch moves the
+    shrink's bytes only (the next sketch reads its tiles on chip)."""
+    if "+" in label:
+        return kernel_bytes(cfg, label.split("+")[0])
     es = 8 if cfg["dtype"] == "f64" else 4
     dims, K = list(cfg["dims"]), list(cfg["K"])
     cur = list(dims)

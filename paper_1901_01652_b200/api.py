@@ -16,6 +16,7 @@ Tensors are numpy arrays in the reference layout (first index fastest, i.e.
 numpy order='F'); all compute runs in libtrg.so on the B200.
 """
 import ctypes
+import weakref
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -83,6 +84,12 @@ class Context:
             L.call("trg_ctx_create_dist", ctypes.c_int(device), ctypes.c_int(rank), ctypes.c_int(world), buf,
                    ctypes.byref(self._h))
         self.device, self.rank, self.world = device, rank, world
+        # handles created on this context; closed before the context itself so that a
+        # child's destructor never runs against a destroyed context (interpreter exit)
+        self._children = weakref.WeakSet()
+
+    def _adopt(self, child):
+        self._children.add(child)
 
     @staticmethod
     def nccl_unique_id():
@@ -126,8 +133,17 @@ class Context:
 
     def close(self):
         if self._h:
+            for child in list(self._children):
+                try:
+                    child.close()
+                except Exception:
+                    pass
             L.call("trg_ctx_destroy", self._h)
             self._h = ctypes.c_void_p()
+
+    @property
+    def alive(self):
+        return bool(self._h)
 
     def __del__(self):
         try:
@@ -173,6 +189,7 @@ class DeviceTensor:
         lo, hi = ctypes.c_int64(), ctypes.c_int64()
         L.call("trg_tensor_info", self._h, None, None, None, ctypes.byref(lo), ctypes.byref(hi))
         self.lo, self.hi = lo.value, hi.value
+        ctx._adopt(self)
 
     @property
     def local_shape(self):
@@ -217,7 +234,8 @@ class DeviceTensor:
 
     def close(self):
         if self._h:
-            L.call("trg_tensor_destroy", self._h)
+            if self.ctx.alive:  # a closed context has already closed its children
+                L.call("trg_tensor_destroy", self._h)
             self._h = ctypes.c_void_p()
 
     def __del__(self):
@@ -240,6 +258,7 @@ class DeviceSketch:
         k, kp = L.i64(self.K)
         L.call("trg_sketch_run", ctx.handle, x.handle, kp, ctypes.c_uint64(spec.seed), ctypes.c_int(variant),
                ctypes.byref(self._h))
+        ctx._adopt(self)
 
     def projected(self):
         out = np.empty(int(np.prod(self.K)), dtype=np.float64)
@@ -278,7 +297,8 @@ class DeviceSketch:
 
     def close(self):
         if self._h:
-            L.call("trg_sketch_destroy", self._h)
+            if self.ctx.alive:
+                L.call("trg_sketch_destroy", self._h)
             self._h = ctypes.c_void_p()
 
     def __del__(self):

@@ -54,6 +54,17 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
 bool stream_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim);
 void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                        cudaStream_t s);
+// ---- fused mode-0 shrink + mode-1 sketch (K3), fp64, left == 1
+struct FusedPlan {
+    int64_t I0, I1, nfib, ldq, K0, K1;  // nfib = local mode-1 fibres = prod of local extents of modes >= 2
+    uint64_t seed, D1;
+    int64_t rows_glob1, col_off1;
+};
+bool fused_ttm_sketch_ok(int dtype, int64_t left, int64_t I0, int64_t K0, int64_t I1, int64_t K1);
+// out = P^(1), y1 = Y_1 (I1 x K1 col-major) via partial (grid x I1 x K1) and a fixed-order sum
+void launch_fused_ttm_sketch(const FusedPlan& p, const void* x, void* out, const double* q, double* partial,
+                             double* y1, int num_sms, cudaStream_t s);
+
 // ---- cp.async-gathered fp64 tensor-core kernels for modes with left > 1 (slab_f64.cu)
 bool slab_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
 void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
@@ -67,6 +78,10 @@ void launch_reduce_partials(const double* partial, int nblocks, int64_t n, doubl
 // ---- thin QR with diag(R) >= 0 (K4): CholQR2 + Householder fallback, fp64.
 // Y is m x k column-major; Q (m x k) out. work >= m*k doubles + 2*k.
 void launch_qr(const double* y, int64_t m, int k, double* q, double* work, int* flag, cudaStream_t s);
+
+// ---- per-device tables of the table-driven Box-Muller (common.cuh), built on first use
+struct GaussTables;
+const GaussTables* gauss_tables(cudaStream_t s);
 
 // ---- Gaussian test-matrix export (parity): out(c, k) = draw off + c + rows*k
 void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, double* out, cudaStream_t s);

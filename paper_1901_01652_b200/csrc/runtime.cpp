@@ -431,13 +431,45 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     };
 
     if (variant == TRG_SEQUENTIAL) {
+        std::vector<bool> y_ready(N, false);
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
-            sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-            sketch_mode(ctx, x, cur, shape, n, Kn, seed, offs[n], sk->dY[n]);
+            if (!y_ready[n]) {
+                sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
+                sketch_mode(ctx, x, cur, shape, n, Kn, seed, offs[n], sk->dY[n]);
+            }
             qr(n);
-            void* out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
+            void* out = nullptr;
+            // K3: fuse this shrink with the next mode's sketch while P^(1) tiles are on chip
+            static const bool no_fuse = getenv("TRG_NO_FUSE") != nullptr;  // A/B switch for profiling
+            if (!no_fuse && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
+                trg::fused_ttm_sketch_ok(x->dtype, 1, shape[0], Kn, shape[1], sk->K[1])) {
+                trg::FusedPlan fp{};
+                fp.I0 = shape[0];
+                fp.I1 = shape[1];
+                fp.nfib = prod(shape, 2);
+                fp.ldq = x->dims[0];
+                fp.K0 = Kn;
+                fp.K1 = sk->K[1];
+                fp.seed = seed;
+                fp.D1 = offs[1].D;
+                fp.rows_glob1 = offs[1].rows_glob;
+                fp.col_off1 = offs[1].col_off;
+                out = ctx->alloc(trg::dtype_size(x->dtype) * (size_t)(Kn * prod(shape, 1)));
+                sk->dY[1] = (double*)ctx->alloc(sizeof(double) * x->dims[1] * sk->K[1]);
+                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(fp.nfib, ctx->num_sms));
+                double* partial = (double*)ctx->alloc(sizeof(double) * grid * fp.I1 * fp.K1);
+                ctx->launch("ttm_m0+sketch_m1", [&] {
+                    trg::launch_fused_ttm_sketch(fp, cur, out, sk->dQ[0], partial, sk->dY[1], ctx->num_sms,
+                                                 ctx->stream);
+                }, 2);
+                ctx->dfree(partial);
+                ctx->allreduce(sk->dY[1], (size_t)(x->dims[1] * sk->K[1]), F64);
+                y_ready[1] = true;
+            } else {
+                out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
+            }
             if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), x->dtype);
             if (owned) ctx->dfree(owned);
             owned = out;

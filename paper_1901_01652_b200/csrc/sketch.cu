@@ -15,6 +15,7 @@
 //   fixed order and each CTA writes one dim x K fp64 partial; a second kernel
 //   sums the partials in CTA order, so the result is bit-reproducible.
 #include <algorithm>
+#include <mutex>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -172,9 +173,28 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restric
     }
 }
 
-__global__ void k_omega(uint64_t seed, uint64_t off, int64_t n, double* out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = gauss_draw<double>(seed, off + (uint64_t)i);
+__global__ void k_gauss_tables(GaussTables* t) {
+    const int i = threadIdx.x;
+    if (i < 128) {
+        const double c = 1.0 + (i + 0.5) / 128.0;
+        t->logt[i] = make_double2(1.0 / c, log(c));
+    }
+    if (i < 256) {
+        double sn, cs;
+        sincospi(2.0 * (i + 0.5) / 256.0, &sn, &cs);
+        t->sct[i] = make_double2(sn, cs);
+    }
+}
+
+// the same table-driven generator the streaming kernels use, so the exported
+// test matrix is exactly what the sketches multiply by
+__global__ void k_omega(uint64_t seed, uint64_t off, int64_t n, double* out, const GaussTables* gt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = off + (uint64_t)i;
+        double z0, z1;
+        gauss_pair_tab(seed, d >> 1, *gt, z0, z1);
+        out[i] = (d & 1ull) ? z1 : z0;
+    }
 }
 
 template <typename T, int TD, int TK, bool L1>
@@ -262,6 +282,21 @@ void launch_sketch(const SketchPlan& p, const void* x, double* partial, double* 
     launch_reduce_partials(partial, p.grid_x, p.dim * p.K, y, s);
 }
 
+const GaussTables* gauss_tables(cudaStream_t s) {
+    static std::mutex mu;
+    static GaussTables* per_dev[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!per_dev[dev]) {
+        GaussTables* t = nullptr;
+        if (cudaMalloc(&t, sizeof(GaussTables)) != cudaSuccess) return nullptr;
+        k_gauss_tables<<<1, 256, 0, s>>>(t);
+        per_dev[dev] = t;
+    }
+    return per_dev[dev];
+}
+
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s) {
     const int blocks = (int)std::max<int64_t>(1, (n + 31) / 32);
     k_reduce_partials<<<blocks, 256, 0, s>>>(partial, nblocks, n, out);
@@ -271,7 +306,7 @@ void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, doubl
     const int64_t n = rows * cols;
     const int threads = 256;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 4096));
-    k_omega<<<blocks, threads, 0, s>>>(seed, off, n, out);
+    k_omega<<<blocks, threads, 0, s>>>(seed, off, n, out, gauss_tables(s));
 }
 
 }  // namespace trg

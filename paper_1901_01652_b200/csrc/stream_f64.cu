@@ -15,6 +15,7 @@
 // straight into MMA-fragment order while the MMAs run. fp64 is kept
 // end to end because the reference is fp64 and the parity bound is 1e-10.
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -26,8 +27,10 @@ namespace trg {
 namespace {
 
 constexpr int kStages = 3;
-constexpr int kCons = 4;  // consumer warps
-constexpr int kRng = 8;   // Omega generator warps (sketch)
+constexpr int kCons = 4;    // consumer warps (shrink)
+constexpr int kSkCons = 8;  // consumer warps (sketch): 2 per SM sub-partition keep the DMMA pipe fed
+constexpr int kRng = 8;     // Omega generator warps (sketch)
+constexpr int kOB = 4;      // Omega tile buffers: the generators may run kOB - 1 tiles ahead
 constexpr int kPad = 8;   // zeroed doubles after each stage (A rows may overrun by < 8)
 constexpr size_t kBarBytes = 256;  // room for the mbarriers after the buffers
 
@@ -37,6 +40,8 @@ struct SkArgs {
     int K, CT, mtiles;
     uint64_t seed, D;
     double* partial;
+    const GaussTables* gt;
+    int dbg;  // TEMP experiment: 1 = skip RNG math, 2 = skip MMAs
 };
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
@@ -46,7 +51,7 @@ __device__ __forceinline__ int omega_idx(int c, int k, int NT) {
 }
 
 template <int MTW, int NT>
-__global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(SkArgs a) {
+__global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(SkArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int CT = a.CT;
     const int64_t dim = a.dim;
@@ -54,31 +59,33 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
     double* stages = reinterpret_cast<double*>(smem_raw);
     const int omega_elems = CT * NT * 8;
     double* omega = stages + kStages * stage_elems;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(omega + 2 * omega_elems);
+    GaussTables* tabs = reinterpret_cast<GaussTables*>(omega + kOB * omega_elems);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tabs + 1);
     uint64_t* full_x = bars;
     uint64_t* empty_x = bars + kStages;
     uint64_t* full_o = bars + 2 * kStages;
-    uint64_t* empty_o = bars + 2 * kStages + 2;
+    uint64_t* empty_o = bars + 2 * kStages + kOB;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nl = (int)((a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
     for (int i = tid; i < kStages * stage_elems; i += blockDim.x) stages[i] = 0.0;
-    for (int i = tid; i < 2 * omega_elems; i += blockDim.x) omega[i] = 0.0;
+    for (int i = tid; i < kOB * omega_elems; i += blockDim.x) omega[i] = 0.0;
+    gauss_tables_to_smem(*tabs, a.gt);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_x[s], 1);
-            mbar_init(&empty_x[s], kCons * 32);
+            mbar_init(&empty_x[s], kSkCons * 32);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kOB; ++b) {
             mbar_init(&full_o[b], kRng * 32);
-            mbar_init(&empty_o[b], kCons * 32);
+            mbar_init(&empty_o[b], kSkCons * 32);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (warp == kCons + kRng) {
+    if (warp == kSkCons + kRng) {
         // ---------------- producer: TMA bulk copies of CT whole columns
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
@@ -95,36 +102,60 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
         }
         return;
     }
-    if (warp >= kCons) {
-        // ---------------- generator warps: Omega tile in B-fragment order
-        const int rt = tid - kCons * 32;
-        const int npmax = CT / 2 + 1;
+    if (warp >= kSkCons) {
+        // ---------------- generator warps: Omega tile in B-fragment order.
+        // Two independent Box-Muller pairs per thread per iteration (ILP 2):
+        // the fp64 log/sqrt/sincospi chains are latency-bound otherwise.
+        const int rt = tid - kSkCons * 32;
+        // pairs per k-column of the tile: CT/2 when every column run starts on an
+        // even draw (then nothing is wasted), one more otherwise
+        const int npmax = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) ? CT / 2 + 1 : CT / 2;
+        const int nitems = a.K * npmax;
         for (int j = 0; j < nl; ++j) {
-            const int b = j & 1;
-            mbar_wait(&empty_o[b], ((j >> 1) & 1) ^ 1);
+            const int b = j % kOB;
+            mbar_wait(&empty_o[b], ((j / kOB) & 1) ^ 1);
             const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
             const int64_t c0 = t * CT;
             const int64_t ncol = imin64(CT, a.ncols - c0);
             double* O = omega + b * omega_elems;
-            for (int it = rt; it < a.K * npmax; it += kRng * 32) {
-                const int k = it / npmax;
-                const int jj = it - k * npmax;
-                const uint64_t s0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)k;
-                const uint64_t p = (s0 >> 1) + (uint64_t)jj;
-                if (p > ((s0 + (uint64_t)CT - 1ull) >> 1)) continue;
-                double z0, z1;
-                gauss_pair(a.seed, p, z0, z1);
-                const int64_t cc = (int64_t)(2ull * p - s0);
-                if (cc >= 0 && cc < CT) O[omega_idx((int)cc, k, NT)] = cc < ncol ? z0 : 0.0;
-                if (cc + 1 >= 0 && cc + 1 < CT) O[omega_idx((int)cc + 1, k, NT)] = cc + 1 < ncol ? z1 : 0.0;
+            for (int it0 = rt; it0 < nitems; it0 += 2 * kRng * 32) {
+                double z[2][2];
+                int kk[2];
+                int64_t cc[2];
+                bool live[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int it = it0 + u * kRng * 32;
+                    const int k = it / npmax;
+                    const int jj = it - k * npmax;
+                    const uint64_t s0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)k;
+                    const uint64_t p = (s0 >> 1) + (uint64_t)jj;
+                    live[u] = it < nitems && p <= ((s0 + (uint64_t)CT - 1ull) >> 1);
+                    kk[u] = k;
+                    cc[u] = (int64_t)(2ull * p - s0);
+                    z[u][0] = 0.5;
+                    z[u][1] = 0.25;
+                    if (a.dbg != 1) gauss_pair_tab(a.seed, live[u] ? p : 0ull, *tabs, z[u][0], z[u][1]);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (!live[u]) continue;
+                    const int64_t c = cc[u];
+                    if (c >= 0 && c < CT) O[omega_idx((int)c, kk[u], NT)] = c < ncol ? z[u][0] : 0.0;
+                    if (c + 1 >= 0 && c + 1 < CT) O[omega_idx((int)c + 1, kk[u], NT)] = c + 1 < ncol ? z[u][1] : 0.0;
+                }
             }
             mbar_arrive(&full_o[b]);
         }
         return;
     }
     // ---------------- consumer warps: Y(d, k) += sum_c X(d, c) Omega(c, k)
-    // Warp w takes k-steps t = w, w + kCons, ... of every tile with full-height
-    // accumulators, so the work is balanced whatever dim is.
+    // Warp w takes k-steps t = (w & 3), (w & 3) + 4, ... of every tile and the
+    // row-tile half (w >> 2) (MTW <= 8 row tiles of 8), so two warps per SM
+    // sub-partition issue DMMAs and the accumulators stay at 4*MTW doubles.
+    const int tg = warp & 3, half = warp >> 2;
+    const int mt0 = half * MTW;
+    const int my_mt = min(MTW, a.mtiles - mt0);
     double acc[MTW][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MTW; ++mt)
@@ -133,19 +164,19 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
     const int q = lane >> 2, r = lane & 3;
     for (int j = 0; j < nl; ++j) {
         const int s = j % kStages;
-        const int b = j & 1;
+        const int b = j % kOB;
         mbar_wait(&full_x[s], (j / kStages) & 1);
-        mbar_wait(&full_o[b], (j >> 1) & 1);
-        const double* X = stages + s * stage_elems + r * dim + q;
+        mbar_wait(&full_o[b], (j / kOB) & 1);
+        const double* X = stages + s * stage_elems + r * dim + q + 8 * mt0;
         const double* O = omega + b * omega_elems;
-        for (int t = warp; t < CT / 4; t += kCons) {
+        for (int t = tg; t < (a.dbg == 2 ? 0 : CT / 4); t += 4) {
             double bv[NT];
 #pragma unroll
             for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
             const double* xrow = X + 4 * t * dim;
 #pragma unroll
             for (int mt = 0; mt < MTW; ++mt) {
-                if (mt < a.mtiles) {
+                if (mt < my_mt) {
                     const double av = xrow[8 * mt];
 #pragma unroll
                     for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av, bv[jn]);
@@ -155,25 +186,29 @@ __global__ void __launch_bounds__((kCons + kRng + 1) * 32, 1) k_sketch_l1_f64(Sk
         mbar_arrive(&empty_x[s]);
         mbar_arrive(&empty_o[b]);
     }
-    // fixed-order reduction of the consumer warps through (consumed) stage 0
-    asm volatile("bar.sync 1, %0;" ::"n"(kCons * 32));
+    // fixed-order reduction over the 4 k-step groups through (consumed) stage 0;
+    // the two halves of a group write disjoint rows
+    asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
     double* red = stages;
-    const int ld = 8 * MTW;
-    for (int w = 0; w < kCons; ++w) {
-        if (warp == w) {
+    const int ld = 8 * a.mtiles;
+    for (int g = 0; g < 4; ++g) {
+        if (tg == g) {
 #pragma unroll
-            for (int mt = 0; mt < MTW; ++mt)
+            for (int mt = 0; mt < MTW; ++mt) {
+                if (mt < my_mt) {
 #pragma unroll
-                for (int jn = 0; jn < NT; ++jn) {
-                    double* p0 = red + (8 * mt + q) + ld * (8 * jn + 2 * r);
-                    *p0 = (w == 0 ? 0.0 : *p0) + acc[mt][jn][0];
-                    p0[ld] = (w == 0 ? 0.0 : p0[ld]) + acc[mt][jn][1];
+                    for (int jn = 0; jn < NT; ++jn) {
+                        double* p0 = red + (8 * (mt0 + mt) + q) + ld * (8 * jn + 2 * r);
+                        *p0 = (g == 0 ? 0.0 : *p0) + acc[mt][jn][0];
+                        p0[ld] = (g == 0 ? 0.0 : p0[ld]) + acc[mt][jn][1];
+                    }
                 }
+            }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kCons * 32));
+        asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
     }
     double* out = a.partial + (int64_t)blockIdx.x * dim * a.K;
-    for (int e = tid; e < dim * a.K; e += kCons * 32) {
+    for (int e = tid; e < dim * a.K; e += kSkCons * 32) {
         const int k = e / (int)dim;
         const int d = e - k * (int)dim;
         out[d + dim * k] = red[d + ld * k];
@@ -283,6 +318,315 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_l1_f64(TtmArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------- fused shrink + next sketch
+// K3: P^(1) = X x_0 Q_0^T and, while each P^(1) tile is still in
+// registers, Y_1 += P^(1)_(1) Omega_1, so P^(1) is written once and never read
+// back for the mode-1 sketch (sketch.hpp:85 followed by :80-83 of mode 1).
+// A work item is one mode-1 fibre f = (i_2, ...) of P^(1): rows m = i_1 + I_1 f
+// of X_(0)^T (I_1 <= 128 rows, processed as H <= 2 row blocks of 64). For that
+// fibre P^(1)_(1) contributes the columns c = o + K_0 f, so
+//   Y_1(i_1, k) += sum_o P1(i_1, o) Omega_1(o + K_0 f, k)
+// is a (rows x K_0)(K_0 x K_1) DMMA whose A fragments come from the shrink's
+// accumulators by quad shuffles and whose B fragments (the K_0 x K_1 block of
+// the reference test matrix) are regenerated per fibre by two generator warps.
+constexpr int kFCons = 4;  // consumer warps: 16 rows each, 64 rows per block
+constexpr int kFGen = 2;   // Omega_1 generator warps
+
+struct FusedArgs {
+    const double* x;     // X, read as rows of I_0
+    double* out;         // P^(1), rows of K_0
+    const double* q;     // Q_0 (ldq x K0 col-major)
+    double* partial;     // per-CTA Y_1 partial (I_1 x K_1 col-major)
+    const GaussTables* gt;
+    int64_t I0, I1, nfib, ldq;
+    int K0, K1, Tk, H, ks;  // ks = ceil(K0 / 4) k-steps of the sketch product
+    uint64_t seed, D1;
+    int64_t rows_glob1, col_off1;
+};
+
+template <int NT0, int NT1>
+__global__ void __launch_bounds__((kFCons + kFGen + 1) * 32, 1) k_ttm_sketch_l1_f64(FusedArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int64_t I0 = a.I0;
+    const int stage_elems = (int)(64 * I0) + kPad;
+    double* stages = reinterpret_cast<double*>(smem_raw);
+    double* Bf = stages + kStages * stage_elems;  // Q_0 in B-fragment order
+    const int bf_elems = a.Tk * NT0 * 32;
+    double* Ob = Bf + bf_elems;  // 2 Omega_1 blocks in B-fragment order
+    const int ob_elems = a.ks * NT1 * 32;
+    GaussTables* tabs = reinterpret_cast<GaussTables*>(Ob + 2 * ob_elems);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tabs + 1);
+    uint64_t* full_x = bars;
+    uint64_t* empty_x = bars + kStages;
+    uint64_t* full_o = bars + 2 * kStages;
+    uint64_t* empty_o = bars + 2 * kStages + 2;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nf = (int)((a.nfib - blockIdx.x + gridDim.x - 1) / gridDim.x);  // fibres of this CTA
+    const int nitems = nf * a.H;
+
+    for (int i = tid; i < kStages * stage_elems; i += blockDim.x) stages[i] = 0.0;
+    for (int i = tid; i < 2 * ob_elems; i += blockDim.x) Ob[i] = 0.0;
+    for (int i = tid; i < bf_elems; i += blockDim.x) {
+        const int t = i / (NT0 * 32);
+        const int jn = (i >> 5) % NT0;
+        const int ln = i & 31;
+        const int64_t d = 4 * t + (ln & 3);
+        const int o = 8 * jn + (ln >> 2);
+        Bf[i] = (d < I0 && o < a.K0) ? a.q[d + a.ldq * o] : 0.0;
+    }
+    gauss_tables_to_smem(*tabs, a.gt);
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_x[s], 1);
+            mbar_init(&empty_x[s], kFCons * 32);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&full_o[b], kFGen * 32);
+            mbar_init(&empty_o[b], kFCons * 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kFCons + kFGen) {
+        // ---------------- producer: one TMA bulk copy per 64-row block of a fibre
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int j = 0; j < nitems; ++j) {
+                const int s = j % kStages;
+                mbar_wait(&empty_x[s], ((j / kStages) & 1) ^ 1);
+                const int64_t f = blockIdx.x + (int64_t)(j / a.H) * gridDim.x;
+                const int h = j % a.H;
+                const int64_t m0 = f * a.I1 + 64 * h;
+                const int64_t nrow = imin64(64, a.I1 - 64 * h);
+                const uint32_t bytes = (uint32_t)(nrow * I0 * 8);
+                mbar_arrive_expect_tx(&full_x[s], bytes);
+                bulk_g2s(stages + s * stage_elems, a.x + m0 * I0, bytes, &full_x[s], pol);
+            }
+        }
+        return;
+    }
+    if (warp >= kFCons) {
+        // ---------------- generators: Omega_1 rows o + K_0 f (o < K_0), all K_1 columns
+        const int gt = tid - kFCons * 32;
+        const int npk = a.K0 / 2 + 1;  // pairs covering K_0 consecutive draws
+        for (int i = 0; i < nf; ++i) {
+            const int b = i & 1;
+            mbar_wait(&empty_o[b], ((i >> 1) & 1) ^ 1);
+            const int64_t f = blockIdx.x + (int64_t)i * gridDim.x;
+            double* O = Ob + b * ob_elems;
+            for (int it = gt; it < a.K1 * npk; it += kFGen * 32) {
+                const int k = it / npk, jj = it - k * npk;
+                const uint64_t s0 = a.D1 + (uint64_t)(a.col_off1 + a.K0 * f) + (uint64_t)a.rows_glob1 * (uint64_t)k;
+                const uint64_t p = (s0 >> 1) + (uint64_t)jj;
+                if (p > ((s0 + (uint64_t)a.K0 - 1ull) >> 1)) continue;
+                double z0, z1;
+                gauss_pair_tab(a.seed, p, *tabs, z0, z1);
+                const int64_t o = (int64_t)(2ull * p - s0);
+                if (o >= 0 && o < a.K0) O[(((o >> 2) * NT1 + (k >> 3)) << 5) + (o & 3) + ((k & 7) << 2)] = z0;
+                if (o + 1 >= 0 && o + 1 < a.K0)
+                    O[((((o + 1) >> 2) * NT1 + (k >> 3)) << 5) + ((o + 1) & 3) + ((k & 7) << 2)] = z1;
+            }
+            mbar_arrive(&full_o[b]);
+        }
+        return;
+    }
+    // ---------------- consumers: warp w owns rows 16w..16w+15 of every 64-row block
+    const int q = lane >> 2, r = lane & 3;
+    double yacc[2][2][NT1][2];  // [row block h][row tile][column tile][pair]
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int jn = 0; jn < NT1; ++jn) yacc[h][mt][jn][0] = yacc[h][mt][jn][1] = 0.0;
+    for (int j = 0; j < nitems; ++j) {
+        const int s = j % kStages;
+        const int i = j / a.H, h = j % a.H;
+        mbar_wait(&full_x[s], (j / kStages) & 1);
+        const double* x0 = stages + s * stage_elems + (16 * warp + q) * I0 + r;
+        const double* x1 = x0 + 8 * I0;
+        double acc[2][NT0][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int jn = 0; jn < NT0; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < a.Tk; ++t) {
+            double bv[NT0];
+#pragma unroll
+            for (int jn = 0; jn < NT0; ++jn) bv[jn] = Bf[((t * NT0 + jn) << 5) + lane];
+            const double a0 = x0[4 * t], a1 = x1[4 * t];
+#pragma unroll
+            for (int jn = 0; jn < NT0; ++jn) {
+                dmma884(acc[0][jn][0], acc[0][jn][1], a0, bv[jn]);
+                dmma884(acc[1][jn][0], acc[1][jn][1], a1, bv[jn]);
+            }
+        }
+        mbar_arrive(&empty_x[s]);
+        const int64_t f = blockIdx.x + (int64_t)i * gridDim.x;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const int row = 64 * h + 16 * warp + 8 * mt + q;  // i_1 of this lane's accumulator row
+            if (row < a.I1) {
+                double* dst = a.out + (f * a.I1 + row) * a.K0;
+#pragma unroll
+                for (int jn = 0; jn < NT0; ++jn) {
+                    const int o = 8 * jn + 2 * r;
+                    if (o + 1 < a.K0 && !(a.K0 & 1)) {
+                        *reinterpret_cast<double2*>(dst + o) = make_double2(acc[mt][jn][0], acc[mt][jn][1]);
+                    } else {
+                        if (o < a.K0) dst[o] = acc[mt][jn][0];
+                        if (o + 1 < a.K0) dst[o + 1] = acc[mt][jn][1];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int jn = 0; jn < NT0; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
+            }
+        }
+        // sketch of the next mode: A(row, o) from the D fragments by quad shuffles
+        const int b = i & 1;
+        if (h == 0) mbar_wait(&full_o[b], (i >> 1) & 1);
+        const double* O = Ob + b * ob_elems;
+#pragma unroll
+        for (int t = 0; t < 2 * NT0; ++t) {
+            if (t < a.ks) {
+                const int src = (lane & ~3) + 2 * (t & 1) + (r >> 1);
+                double av[2];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const double v0 = __shfl_sync(0xffffffffu, acc[mt][t >> 1][0], src);
+                    const double v1 = __shfl_sync(0xffffffffu, acc[mt][t >> 1][1], src);
+                    av[mt] = (r & 1) ? v1 : v0;
+                }
+#pragma unroll
+                for (int jn = 0; jn < NT1; ++jn) {
+                    const double bo = O[((t * NT1 + jn) << 5) + lane];
+                    if (h == 0) {
+                        dmma884(yacc[0][0][jn][0], yacc[0][0][jn][1], av[0], bo);
+                        dmma884(yacc[0][1][jn][0], yacc[0][1][jn][1], av[1], bo);
+                    } else {
+                        dmma884(yacc[1][0][jn][0], yacc[1][0][jn][1], av[0], bo);
+                        dmma884(yacc[1][1][jn][0], yacc[1][1][jn][1], av[1], bo);
+                    }
+                }
+            }
+        }
+        if (h == a.H - 1) mbar_arrive(&empty_o[b]);
+    }
+    // per-CTA Y_1 partial: rows are disjoint across warps, no reduction needed
+    double* outp = a.partial + (int64_t)blockIdx.x * a.I1 * a.K1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const int row = 64 * h + 16 * warp + 8 * mt + q;
+            if (h >= a.H || row >= a.I1) continue;
+#pragma unroll
+            for (int jn = 0; jn < NT1; ++jn) {
+                const int k = 8 * jn + 2 * r;
+                if (k < a.K1) outp[row + a.I1 * k] = yacc[h][mt][jn][0];
+                if (k + 1 < a.K1) outp[row + a.I1 * (k + 1)] = yacc[h][mt][jn][1];
+            }
+        }
+}
+
+
+// Shrink with the small operand in registers: out^T (o x rows) = Q^T (o x d) X^T.
+// Q^T is the DMMA A operand and stays in registers for the whole kernel (TKM x
+// MTO fragments), so shared memory only feeds the X^T B fragments: one LDS.64
+// per 2*MTO DMMAs (half the smem traffic of the X-as-A form, which is what
+// bounds the fp64 tensor pipe here). Warp w owns rows 16w..16w+15 of a tile.
+template <int MTO, int TKM>
+__global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int64_t dim = a.dim;
+    const int MT = a.MT;
+    const int stage_elems = (int)(MT * dim) + kPad;
+    double* stages = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * stage_elems);
+    uint64_t* full_x = bars;
+    uint64_t* empty_x = bars + kStages;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nl = (int)((a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int q = lane >> 2, r = lane & 3;
+
+    for (int i = tid; i < kStages * stage_elems; i += blockDim.x) stages[i] = 0.0;
+    // A fragments of Q^T: qa[mt][t] = Q^T(o = 8 mt + q, d = 4 t + r) = Q(d, o)
+    double qa[MTO][TKM];
+#pragma unroll
+    for (int mt = 0; mt < MTO; ++mt)
+#pragma unroll
+        for (int t = 0; t < TKM; ++t) {
+            const int64_t d = 4 * t + r;
+            const int o = 8 * mt + q;
+            qa[mt][t] = (t < a.Tk && d < dim && o < a.K) ? a.q[d + a.ldq * o] : 0.0;
+        }
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_x[s], 1);
+            mbar_init(&empty_x[s], kCons * 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kCons) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int j = 0; j < nl; ++j) {
+                const int s = j % kStages;
+                mbar_wait(&empty_x[s], ((j / kStages) & 1) ^ 1);
+                const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
+                const int64_t m0 = t * MT;
+                const int64_t nrow = imin64(MT, a.rows - m0);
+                const uint32_t bytes = (uint32_t)(nrow * dim * 8);
+                mbar_arrive_expect_tx(&full_x[s], bytes);
+                bulk_g2s(stages + s * stage_elems, a.x + m0 * dim, bytes, &full_x[s], pol);
+            }
+        }
+        return;
+    }
+    for (int j = 0; j < nl; ++j) {
+        const int s = j % kStages;
+        mbar_wait(&full_x[s], (j / kStages) & 1);
+        // B fragment: X^T(d = 4t + r, row = 8 nt + q) = X[row][d]
+        const double* x0 = stages + s * stage_elems + (16 * warp + q) * dim + r;
+        const double* x1 = x0 + 8 * dim;
+        double acc[MTO][2][2];
+#pragma unroll
+        for (int mt = 0; mt < MTO; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
+#pragma unroll
+        for (int t = 0; t < TKM; ++t) {
+            if (t < a.Tk) {
+                const double b0 = x0[4 * t], b1 = x1[4 * t];
+#pragma unroll
+                for (int mt = 0; mt < MTO; ++mt) {
+                    dmma884(acc[mt][0][0], acc[mt][0][1], qa[mt][t], b0);
+                    dmma884(acc[mt][1][0], acc[mt][1][1], qa[mt][t], b1);
+                }
+            }
+        }
+        mbar_arrive(&empty_x[s]);
+        // D fragment: out^T(o = 8 mt + q, row = 16 w + 8 nt + 2 r + e)
+        const int64_t m0 = (blockIdx.x + (int64_t)j * gridDim.x) * MT + 16 * warp;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t m = m0 + 8 * nt + 2 * r + e;
+                if (m >= a.rows) continue;
+#pragma unroll
+                for (int mt = 0; mt < MTO; ++mt) {
+                    const int o = 8 * mt + q;
+                    if (o < a.K) a.out[m * a.K + o] = acc[mt][nt][e];
+                }
+            }
+    }
+}
+
 int nt_for(int K) {
     const int nt = (K + 7) / 8;
     return nt <= 1 ? 1 : nt <= 2 ? 2 : nt <= 4 ? 4 : 8;
@@ -300,8 +644,12 @@ constexpr size_t kSmemBudget = 220 * 1024;
 // ---------------------------------------------------------------- sketch
 bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
     if (dtype != F64 || left != 1 || (dim & 1) || K > 64 || dim > 128) return false;
+    // register budget at 17 warps/SM: (row tiles per warp) x (8-column groups) accumulators
+    const int mtw = (int)((dim + 7) / 8 + 1) / 2;
+    if (nt_for(K) > 4 || (nt_for(K) == 4 && mtw > 4)) return false;
     const int CT = dim <= 112 ? 64 : 32;
-    const size_t smem = (kStages * (size_t)(CT * dim + kPad) + 2 * (size_t)CT * nt_for(K) * 8) * 8 + kBarBytes;
+    const size_t smem =
+        (kStages * (size_t)(CT * dim + kPad) + kOB * (size_t)CT * nt_for(K) * 8) * 8 + sizeof(GaussTables) + kBarBytes;
     return smem <= kSmemBudget;
 }
 
@@ -320,12 +668,15 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.seed = p.seed;
     a.D = p.D;
     a.partial = partial;
+    a.dbg = getenv("TRG_DEBUG_SKETCH") ? atoi(getenv("TRG_DEBUG_SKETCH")) : 0;
+    a.gt = gauss_tables(s);
     const int NT = nt_for(p.K);
-    const int mtw = a.mtiles;  // full-height accumulators per consumer warp
-    const size_t smem = (kStages * (size_t)(a.CT * a.dim + kPad) + 2 * (size_t)a.CT * NT * 8) * 8 + kBarBytes;
+    const int mtw = (a.mtiles + 1) / 2;  // row tiles per consumer warp (two halves)
+    const size_t smem =
+        (kStages * (size_t)(a.CT * a.dim + kPad) + kOB * (size_t)a.CT * NT * 8) * 8 + sizeof(GaussTables) + kBarBytes;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     *grid_out = grid;
-    const int threads = (kCons + kRng + 1) * 32;
+    const int threads = (kSkCons + kRng + 1) * 32;
 #define TRG_SK(MTW, NTV)                                                 \
     do {                                                                 \
         set_smem(k_sketch_l1_f64<MTW, NTV>, smem);                       \
@@ -338,14 +689,14 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
         case 4: TRG_SK(MTW, 4); break;   \
         default: TRG_SK(MTW, 8); break;  \
     }
-    if (mtw <= 4) {
+    if (mtw <= 2) {
+        TRG_SK_NT(2)
+    } else if (mtw <= 4) {
         TRG_SK_NT(4)
-    } else if (mtw <= 8) {
-        TRG_SK_NT(8)
-    } else if (mtw <= 13) {
-        TRG_SK_NT(13)
+    } else if (mtw <= 7) {
+        TRG_SK_NT(7)
     } else {
-        TRG_SK_NT(16)
+        TRG_SK_NT(8)
     }
 #undef TRG_SK_NT
 #undef TRG_SK
@@ -374,15 +725,82 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
     a.Tk = (int)((p.dim + 3) / 4);
     a.ntiles = (a.rows + a.MT - 1) / a.MT;
     const int NT = nt_for(a.K);
-    const size_t smem = (kStages * (size_t)(a.MT * a.dim + kPad) + (size_t)a.Tk * NT * 32) * 8 + kBarBytes;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     const int threads = (kCons + 1) * 32;
+    if (a.K <= 16 && a.Tk <= 32) {  // Q^T resident in registers
+        const size_t smem = kStages * (size_t)(a.MT * a.dim + kPad) * 8 + kBarBytes;
+#define TRG_QR(MTO, TKM)                                                  \
+    do {                                                                  \
+        set_smem(k_ttm_qreg_f64<MTO, TKM>, smem);                         \
+        k_ttm_qreg_f64<MTO, TKM><<<grid, threads, smem, s>>>(a);          \
+    } while (0)
+        if (a.K <= 8) {
+            if (a.Tk <= 16) TRG_QR(1, 16); else if (a.Tk <= 25) TRG_QR(1, 25); else TRG_QR(1, 32);
+        } else {
+            if (a.Tk <= 16) TRG_QR(2, 16); else if (a.Tk <= 25) TRG_QR(2, 25); else TRG_QR(2, 32);
+        }
+#undef TRG_QR
+        return;
+    }
+    const size_t smem = (kStages * (size_t)(a.MT * a.dim + kPad) + (size_t)a.Tk * NT * 32) * 8 + kBarBytes;
     switch (NT) {
         case 1: set_smem(k_ttm_l1_f64<1>, smem); k_ttm_l1_f64<1><<<grid, threads, smem, s>>>(a); break;
         case 2: set_smem(k_ttm_l1_f64<2>, smem); k_ttm_l1_f64<2><<<grid, threads, smem, s>>>(a); break;
         case 4: set_smem(k_ttm_l1_f64<4>, smem); k_ttm_l1_f64<4><<<grid, threads, smem, s>>>(a); break;
         default: set_smem(k_ttm_l1_f64<8>, smem); k_ttm_l1_f64<8><<<grid, threads, smem, s>>>(a); break;
     }
+}
+
+}  // namespace trg
+
+namespace trg {
+
+bool fused_ttm_sketch_ok(int dtype, int64_t left, int64_t I0, int64_t K0, int64_t I1, int64_t K1) {
+    if (dtype != F64 || left != 1 || (I0 & 1) || I0 > 128 || I1 > 128 || K0 > 16 || K1 > 16) return false;
+    const int Tk = (int)((I0 + 3) / 4);
+    const size_t smem = (kStages * (size_t)(64 * I0 + kPad) + (size_t)Tk * 2 * 32 + 2 * 4 * 2 * 32) * 8 +
+                        sizeof(GaussTables) + kBarBytes;
+    return smem <= kSmemBudget;
+}
+
+void launch_fused_ttm_sketch(const FusedPlan& p, const void* x, void* out, const double* q, double* partial,
+                             double* y1, int num_sms, cudaStream_t s) {
+    FusedArgs a;
+    a.x = reinterpret_cast<const double*>(x);
+    a.out = reinterpret_cast<double*>(out);
+    a.q = q;
+    a.ldq = p.ldq;
+    a.partial = partial;
+    a.gt = gauss_tables(s);
+    a.I0 = p.I0;
+    a.I1 = p.I1;
+    a.nfib = p.nfib;
+    a.K0 = (int)p.K0;
+    a.K1 = (int)p.K1;
+    a.Tk = (int)((p.I0 + 3) / 4);
+    a.H = (int)((p.I1 + 63) / 64);
+    a.ks = (int)((p.K0 + 3) / 4);
+    a.seed = p.seed;
+    a.D1 = p.D1;
+    a.rows_glob1 = p.rows_glob1;
+    a.col_off1 = p.col_off1;
+    const int NT0 = a.K0 <= 8 ? 1 : 2;
+    const int NT1 = a.K1 <= 8 ? 1 : 2;
+    const size_t smem = (kStages * (size_t)(64 * a.I0 + kPad) + (size_t)a.Tk * NT0 * 32 + 2 * (size_t)a.ks * NT1 * 32) * 8 +
+                        sizeof(GaussTables) + kBarBytes;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nfib, num_sms));
+    const int threads = (kFCons + kFGen + 1) * 32;
+#define TRG_FZ(A, B)                                                          \
+    do {                                                                      \
+        set_smem(k_ttm_sketch_l1_f64<A, B>, smem);                            \
+        k_ttm_sketch_l1_f64<A, B><<<grid, threads, smem, s>>>(a);             \
+    } while (0)
+    if (NT0 == 1 && NT1 == 1) TRG_FZ(1, 1);
+    else if (NT0 == 1) TRG_FZ(1, 2);
+    else if (NT1 == 1) TRG_FZ(2, 1);
+    else TRG_FZ(2, 2);
+#undef TRG_FZ
+    launch_reduce_partials(partial, grid, p.I1 * p.K1, y1, s);
 }
 
 }  // namespace trg

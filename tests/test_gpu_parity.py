@@ -263,5 +263,6 @@ def test_launch_counter_and_profiling(trg, ctx):
     sk.projected()
     ctx.set_profiling(False)
     labels = ctx.kernel_labels()
-    assert "sketch_m0" in labels and "ttm_m0" in labels and "qr" in labels
-    assert ctx.launch_count() >= 12  # 3 modes x (sketch + reduce + qr + ttm)
+    assert "sketch_m0" in labels and "qr" in labels
+    assert "ttm_m0" in labels or "ttm_m0+sketch_m1" in labels  # fused shrink + next sketch (K3)
+    assert ctx.launch_count() >= 10  # 3 modes x (sketch + reduce + qr + ttm), minus fused launches
