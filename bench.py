@@ -351,7 +351,9 @@ def main():
         k["share"] = k["total_ms"] / prof_total
         del k["total_ms"]
     peak, peak_src = measured_peak()
-    dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"])
+    # dominant kernel among the streaming passes (those with algorithmic bytes)
+    cands = [k for k in kernels if kernel_bytes(cfg, k)] or list(kernels)
+    dom = max(cands, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"])
     kb = kernel_bytes(cfg, dom)
     # local bytes per launch under sharding
     kb_local = kb / world if kb else None

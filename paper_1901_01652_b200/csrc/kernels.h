@@ -72,6 +72,16 @@ void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, dou
 bool slab_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim, int64_t ncols);
 void launch_slab_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                      cudaStream_t s);
+// ---- TMA-tensor (128B-swizzled) fp64 kernels for modes with left > 1 (slab_tma.cu)
+bool slab2_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right);
+int64_t slab2_units(int64_t left, int64_t right);
+// unit blocks of the reference test matrix (4 x NT x 32 doubles per unit), L2-resident
+void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
+                        int64_t rows_glob, double* out, cudaStream_t s);
+void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
+                         int num_sms, cudaStream_t s);
+void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
+                      cudaStream_t s);
 // fixed-order sum of nblocks partial (n doubles each)
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s);
 

@@ -135,6 +135,7 @@ struct trg_ctx {
     int rank = 0, world = 1;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // test-matrix generation for later modes, overlapped with QR / shrink
     ncclComm_t comm = nullptr;
     bool profiling = false;
     int64_t launches = 0;
@@ -325,8 +326,14 @@ std::vector<ModeOffsets> sketch_offsets(const std::vector<int64_t>& dims, const 
 
 // Y_n of the (local) current tensor cur with shape cur_shape, into dYfull
 // (I_n x K_n, replicated).
+// Omega_n unit blocks generated ahead of time on the side stream (slab2 modes)
+struct PreOmega {
+    double* buf = nullptr;
+    cudaEvent_t ready = nullptr;
+};
+
 void sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
-                 int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull) {
+                 int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull, PreOmega* pre = nullptr) {
     const int N = (int)cur_shape.size();
     trg::SketchPlan p{};
     p.dtype = x->dtype;
@@ -347,6 +354,25 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_stream_sketch(p, cur, partial, ylocal, ctx->num_sms, &grid, ctx->stream);
         }, 2);
+    } else if (p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        const int NT = Kn <= 8 ? 1 : 2;
+        double* om = nullptr;
+        if (pre && pre->buf) {
+            om = pre->buf;
+            CK(cudaStreamWaitEvent(ctx->stream, pre->ready, 0));
+        } else {
+            om = (double*)ctx->alloc(sizeof(double) * trg::slab2_units(p.left, p.right) * 4 * NT * 32);
+            ctx->launch("omega_m" + std::to_string(n), [&] {
+                trg::launch_omega_units(p.left, p.right, (int)Kn, p.seed, p.D, p.col_off, p.rows_glob, om,
+                                        ctx->stream);
+            }, 2);
+        }
+        partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_slab2_sketch(p, cur, om, partial, ylocal, ctx->num_sms, ctx->stream);
+        }, 2);
+        ctx->dfree(om);
+        if (pre) pre->buf = nullptr;
     } else if (trg::slab_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.left * p.right)) {
         partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
         ctx->launch("sketch_m" + std::to_string(n), [&] {
@@ -388,6 +414,10 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
         });
+    } else if (p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_slab2_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
+        });
     } else if (trg::slab_ttm_ok(p.dtype, p.left, p.dim, Kn, p.left * p.right)) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_slab_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
@@ -397,6 +427,34 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
         ctx->launch("ttm_m" + std::to_string(n), [&] { trg::launch_ttm(p, cur, out, m, ctx->stream); });
     }
     return out;
+}
+
+void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, const std::vector<int64_t>& K, uint64_t seed,
+                        const std::vector<ModeOffsets>& offs, int after, std::vector<PreOmega>& pre) {
+    const int N = (int)x->dims.size();
+    std::vector<int64_t> shape = x->local_shape();
+    for (int m = 0; m <= after; ++m) shape[m] = K[m];
+    cudaEvent_t go;
+    CK(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+    CK(cudaEventRecord(go, ctx->stream));  // buffers below are allocated on the main stream
+    for (int m = after + 1; m < N; ++m) {
+        if (offs[m].skipped) continue;
+        const int64_t left = prod(shape, 0, m), dim = shape[m], right = prod(shape, m + 1);
+        if (left > 1 && trg::slab2_ok(x->dtype, left, dim, K[m], right)) {
+            const int NT = K[m] <= 8 ? 1 : 2;
+            pre[m].buf = (double*)ctx->alloc(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
+            CK(cudaEventRecord(go, ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->side, go, 0));
+            trg::launch_omega_units(left, right, (int)K[m], seed, offs[m].D, offs[m].col_off, offs[m].rows_glob,
+                                    pre[m].buf, ctx->side);
+            CK(cudaGetLastError());
+            ctx->launches += 2;
+            CK(cudaEventCreateWithFlags(&pre[m].ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(pre[m].ready, ctx->side));
+        }
+        shape[m] = K[m];
+    }
+    CK(cudaEventDestroy(go));
 }
 
 void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk) {
@@ -430,6 +488,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         ctx->dfree(work);
     };
 
+    std::vector<PreOmega> pre(N);
+    bool pre_started = false;
     if (variant == TRG_SEQUENTIAL) {
         std::vector<bool> y_ready(N, false);
         for (int n = 0; n < N; ++n) {
@@ -437,13 +497,21 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
             if (!y_ready[n]) {
                 sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-                sketch_mode(ctx, x, cur, shape, n, Kn, seed, offs[n], sk->dY[n]);
+                sketch_mode(ctx, x, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n]);
+            }
+            if (!pre_started) {
+                // Omega_m of every later slab-kernel mode depends only on shapes and the seed:
+                // generate them on the side stream while this mode's QR (one SM) and
+                // shrink (HBM-bound) run on the main stream
+                pre_started = true;
+                schedule_pre_omega(ctx, x, sk->K, seed, offs, n, pre);
             }
             qr(n);
             void* out = nullptr;
             // K3: fuse this shrink with the next mode's sketch while P^(1) tiles are on chip
-            static const bool no_fuse = getenv("TRG_NO_FUSE") != nullptr;  // A/B switch for profiling
-            if (!no_fuse && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
+            // off by default: the separate shrink + TMA slab sketch measure faster (profiles/)
+            static const bool fuse = getenv("TRG_FUSE") != nullptr;
+            if (fuse && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
                 trg::fused_ttm_sketch_ok(x->dtype, 1, shape[0], Kn, shape[1], sk->K[1])) {
                 trg::FusedPlan fp{};
                 fp.I0 = shape[0];
@@ -520,6 +588,10 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     } else {
         sk->dP = const_cast<void*>(cur);  // no mode projected: P is x itself (sketch.hpp:71)
         sk->P_is_view = true;
+    }
+    for (auto& po : pre) {
+        if (po.buf) ctx->dfree(po.buf);  // mode not reached (cannot happen unless it failed validation)
+        if (po.ready) cudaEventDestroy(po.ready);  // destruction is deferred until the event completes
     }
     CK(cudaEventRecord(sk->ev1, ctx->stream));
 }
@@ -823,6 +895,7 @@ static void ctx_init(trg_ctx* c, int device) {
     if (major != 10) throw nodev_error("libtrg is built for sm_100a (B200); device has compute capability major " +
                                        std::to_string(major));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     CK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
@@ -874,6 +947,8 @@ int trg_ctx_destroy(trg_ctx* ctx) {
         }
         for (auto e : ctx->event_pool) cudaEventDestroy(e);
         if (ctx->comm) nccl().commDestroy(ctx->comm);
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

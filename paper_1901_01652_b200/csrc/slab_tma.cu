@@ -1,0 +1,429 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// fp64 kernels for the modes n >= 1 of the sequential projection, built on TMA
+// tensor copies with the 128-byte hardware swizzle.
+//
+// The working tensor P^(n) is read as a 2-D tensor [rows = dim * right][left]
+// (tensor.hpp:112-123: (left, dim, right), first index fastest). A work unit is
+// u = (r, lc): one slab index r and one 16-wide chunk lc of the left index, i.e.
+// the box {16 x dim} at (16 lc, dim r), which TMA lands in shared memory as
+// dim rows of 128 B, 16-byte chunks XOR-swizzled by (row mod 8). Unfolding
+// column c = l + left r (tensor.hpp:133-142) of unit u is l = 16 lc + (0..15).
+//
+//   k_slab2_sketch_f64  Y_n += X_(n) Omega_n            (sketch.hpp:80-83)
+//       DMMA with A = X^T (rows d, contraction over the 16 l of the unit):
+//       a fragment touches 8 rows x 4 consecutive l, which the swizzle spreads
+//       over all 32 banks (two wavefronts, the minimum for 32 x 8 B).
+//       B = the unit's 16 x K block of the reference test matrix, precomputed
+//       by k_omega_units (L2-resident, 16 % of the tensor) and copied next to
+//       the X box by the same producer into the same stage.
+//   k_slab2_ttm_f64     P^(n+1) = P^(n) x_n Q_n^T       (sketch.hpp:85)
+//       DMMA with A = X (rows l, contraction over d), B = Q_n held in registers
+//       for the whole kernel. The contraction order inside each 4-wide k-step is
+//       permuted (d = 8(t/2) + 2(t%2) + {0,4,1,5}) so that the 4 rows of a
+//       fragment fall into both halves of the swizzle pattern: conflict-free.
+//
+// One producer thread issues the TMA copies into an S-stage mbarrier ring; each
+// of the 4 consumer warps takes whole units (stage j goes to warp j % 4).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "pipeline.cuh"
+
+namespace trg {
+
+namespace {
+
+constexpr int kTCons = 8;    // consumer warps: pairs (w, w + 4) share a unit, two per SM sub-partition
+constexpr int kStg = 8;      // stages (units in flight)
+constexpr int kUnitL = 16;   // left-chunk width of a unit (16 doubles = 128 B rows)
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// element (row d, column l < 16) of a 128B-swizzled stage, in doubles
+__device__ __forceinline__ int swz(int d, int l) { return d * 16 + ((((l >> 1) ^ (d & 7))) << 1) + (l & 1); }
+
+struct Slab2Args {
+    int64_t left, dim, right;  // local view
+    int LC;                    // ceil(left / 16) chunks per slab index
+    int64_t nunits;            // right * LC
+    int K, mtiles, Tk;
+    double* partial;           // sketch: per-CTA Y partial (dim x K)
+    const double* omega;       // sketch: unit blocks of 4 x NT x 32 doubles
+    double* out;               // ttm
+    const double* q;           // ttm: Q (ldq x K col-major)
+    int64_t ldq;
+};
+
+// ------------------------------------------------------------------ test-matrix unit blocks
+// block u, element (t, jn, lane) = Omega(c, k), c = 16 lc + 4 t + (lane & 3) (zero past
+// `left`), k = 8 jn + (lane >> 2) (zero past K); Omega(c, k) = reference draw
+// D + col_off + c + left r + rows_glob k (sketch.hpp:32-38).
+// One CTA iteration per unit, one thread per (k, pair) slot of it: no 64-bit
+// division in the per-draw path (the unit -> (r, lc) split is once per unit).
+__global__ void k_omega_units(int64_t left, int LC, int64_t nunits, int K, int NT, uint64_t seed, uint64_t D,
+                              int64_t col_off, int64_t rows_glob, const GaussTables* gt, double* out) {
+    __shared__ GaussTables tabs;
+    gauss_tables_to_smem(tabs, gt);
+    __syncthreads();
+    constexpr int npp = kUnitL / 2 + 1;  // pairs covering 16 consecutive draws
+    const int slot = threadIdx.x;
+    const int k = slot / npp, jj = slot - k * npp;
+    if (k >= K) return;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t r = LC == 1 ? u : u / LC;
+        const int lc = (int)(u - r * LC);
+        const uint64_t s0 = D + (uint64_t)(col_off + kUnitL * lc + left * r) + (uint64_t)rows_glob * (uint64_t)k;
+        const uint64_t p = (s0 >> 1) + (uint64_t)jj;
+        if (p > ((s0 + kUnitL - 1) >> 1)) continue;
+        double z[2];
+        gauss_pair_tab(seed, p, tabs, z[0], z[1]);
+        double* blk = out + u * (int64_t)(4 * NT * 32);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int l = (int)(2ull * p - s0) + e;  // 0..15 within the unit
+            if (l < 0 || l >= kUnitL) continue;
+            const bool live = kUnitL * lc + l < left;
+            blk[(((l >> 2) * NT + (k >> 3)) << 5) + (l & 3) + ((k & 7) << 2)] = live ? z[e] : 0.0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ sketch
+template <int MTW, int NT>
+__global__ void __launch_bounds__((kTCons + 1) * 32, 1)
+    k_slab2_sketch_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int dim = (int)a.dim;
+    const int rows_pad = (dim + 7) & ~7;
+    const int xbytes = rows_pad * 128;  // multiple of 1024: keeps every stage swizzle-aligned
+    const int obytes = 4 * NT * 32 * 8;
+    const int sbytes = xbytes + ((obytes + 1023) & ~1023);
+    // dynamic smem is only guaranteed 16-B aligned: align the ring to 1024 B by hand
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStg * sbytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStg;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nl = (a.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    // rows dim..rows_pad-1 are never written by TMA: zero them once (their products land in
+    // accumulator rows that are dropped, but must stay finite)
+    for (int i = tid; i < kStg * sbytes / 8; i += blockDim.x) reinterpret_cast<double*>(base)[i] = 0.0;
+    if (tid == 0) {
+        for (int s = 0; s < kStg; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 64);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kTCons) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int64_t j = 0; j < nl; ++j) {
+                const int s = (int)(j % kStg);
+                mbar_wait(&empty[s], (uint32_t)((j / kStg) & 1) ^ 1u);
+                const int64_t u = blockIdx.x + j * gridDim.x;
+                const int64_t r = u / a.LC;
+                const int lc = (int)(u - r * a.LC);
+                unsigned char* st = base + s * sbytes;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128 + obytes));
+                tma_load_2d(st, &tmap, kUnitL * lc, (int)(a.dim * r), &full[s], pol);
+                bulk_g2s(st + xbytes, a.omega + u * (int64_t)(4 * NT * 32), (uint32_t)obytes, &full[s], pol);
+            }
+        }
+        return;
+    }
+    const int q = lane >> 2, rl = lane & 3;
+    const int pair = warp & 3, half = warp >> 2;  // pair takes units j = pair (mod 4); half takes 8-row tiles
+    const int mt0 = half * MTW;
+    const int my_mt = min(MTW, a.mtiles - mt0);
+    double acc[MTW][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MTW; ++mt)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
+    for (int64_t j = pair; j < nl; j += 4) {
+        const int s = (int)(j % kStg);
+        mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
+        const double* X = reinterpret_cast<const double*>(base + s * sbytes);
+        const double* O = reinterpret_cast<const double*>(base + s * sbytes + xbytes);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            double bv[NT];
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
+            const int l = 4 * t + rl;
+#pragma unroll
+            for (int mt = 0; mt < MTW; ++mt) {
+                if (mt < my_mt) {
+                    const double av = X[swz(8 * (mt0 + mt) + q, l)];
+#pragma unroll
+                    for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av, bv[jn]);
+                }
+            }
+        }
+        __syncwarp();
+        mbar_arrive(&empty[s]);
+    }
+    // fixed-order sum of the consumer warps' partials through stage 0 (all consumed)
+    asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
+    double* red = reinterpret_cast<double*>(base);
+    const int ld = 8 * a.mtiles;
+    for (int g = 0; g < 4; ++g) {  // the two halves of a pair write disjoint rows
+        if (pair == g) {
+#pragma unroll
+            for (int mt = 0; mt < MTW; ++mt) {
+                if (mt < my_mt) {
+#pragma unroll
+                    for (int jn = 0; jn < NT; ++jn) {
+                        double* p0 = red + (8 * (mt0 + mt) + q) + ld * (8 * jn + 2 * rl);
+                        *p0 = (g == 0 ? 0.0 : *p0) + acc[mt][jn][0];
+                        p0[ld] = (g == 0 ? 0.0 : p0[ld]) + acc[mt][jn][1];
+                    }
+                }
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
+    }
+    double* outp = a.partial + (int64_t)blockIdx.x * a.dim * a.K;
+    for (int e = tid; e < dim * a.K; e += kTCons * 32) {
+        const int k = e / dim;
+        const int d = e - k * dim;
+        outp[d + a.dim * k] = red[d + ld * k];
+    }
+}
+
+// ------------------------------------------------------------------ shrink
+// contraction order inside k-step t: d = 8 (t / 2) + 2 (t % 2) + perm[r]
+__device__ __forceinline__ int perm_d(int t, int r) { return 8 * (t >> 1) + 2 * (t & 1) + ((r & 1) ? 4 : 0) + (r >> 1); }
+
+template <int NT, int TKM>
+__global__ void __launch_bounds__((kTCons + 1) * 32, 1)
+    k_slab2_ttm_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int dim = (int)a.dim;
+    const int rows_pad = (dim + 7) & ~7;
+    const int sbytes = rows_pad * 128;
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStg * sbytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStg;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nl = (a.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int q = lane >> 2, rl = lane & 3;
+    for (int i = tid; i < kStg * sbytes / 8; i += blockDim.x) reinterpret_cast<double*>(base)[i] = 0.0;
+    // B fragments of Q in registers: qb[t][jn] = Q(d = perm_d(t, rl), o = 8 jn + q)
+    double qb[TKM][NT];
+#pragma unroll
+    for (int t = 0; t < TKM; ++t)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) {
+            const int d = perm_d(t, rl);
+            const int o = 8 * jn + q;
+            qb[t][jn] = (t < a.Tk && d < dim && o < a.K) ? a.q[d + a.ldq * o] : 0.0;
+        }
+    if (tid == 0) {
+        for (int s = 0; s < kStg; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 64);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kTCons) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int64_t j = 0; j < nl; ++j) {
+                const int s = (int)(j % kStg);
+                mbar_wait(&empty[s], (uint32_t)((j / kStg) & 1) ^ 1u);
+                const int64_t u = blockIdx.x + j * gridDim.x;
+                const int64_t r = u / a.LC;
+                const int lc = (int)(u - r * a.LC);
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128));
+                tma_load_2d(base + s * sbytes, &tmap, kUnitL * lc, (int)(a.dim * r), &full[s], pol);
+            }
+        }
+        return;
+    }
+    const int pair = warp & 3, mt = warp >> 2;  // pair takes units j = pair (mod 4); mt = 8-row tile of l
+    for (int64_t j = pair; j < nl; j += 4) {
+        const int s = (int)(j % kStg);
+        mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
+        const double* X = reinterpret_cast<const double*>(base + s * sbytes);
+        double acc[2][NT][2];  // [k-step parity][column tile][pair]
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) acc[p][jn][0] = acc[p][jn][1] = 0.0;
+#pragma unroll
+        for (int t = 0; t < TKM; ++t) {
+            if (t < a.Tk) {
+                const double av = X[swz(perm_d(t, rl), 8 * mt + q)];
+#pragma unroll
+                for (int jn = 0; jn < NT; ++jn) dmma884(acc[t & 1][jn][0], acc[t & 1][jn][1], av, qb[t][jn]);
+            }
+        }
+        __syncwarp();
+        mbar_arrive(&empty[s]);
+        const int64_t u = blockIdx.x + j * gridDim.x;
+        const int64_t r = u / a.LC;
+        const int lc = (int)(u - r * a.LC);
+        // D fragment: (l = 8 mt + q, o = 8 jn + 2 rl + e) -> out(l_glob, o, r) at l + left (o + K r)
+        const int64_t l = (int64_t)kUnitL * lc + 8 * mt + q;
+        if (l < a.left) {
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int o = 8 * jn + 2 * rl + e;
+                    if (o < a.K) a.out[l + a.left * (o + (int64_t)a.K * r)] = acc[0][jn][e] + acc[1][jn][e];
+                }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static std::once_flag once;
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// [rows][left] fp64 view, box {16, dim}, 128B swizzle, zero fill out of bounds
+bool make_map(CUtensorMap* m, const void* x, int64_t left, int64_t rows, int64_t dim) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t gdim[2] = {(cuuint64_t)left, (cuuint64_t)rows};
+    const cuuint64_t gstride[1] = {(cuuint64_t)left * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)kUnitL, (cuuint32_t)dim};
+    const cuuint32_t estride[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(x), gdim, gstride, box, estride,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t sketch_smem(int64_t dim, int NT) {
+    const int rows_pad = (int)((dim + 7) & ~7);
+    const int obytes = 4 * NT * 32 * 8;
+    return (size_t)kStg * (rows_pad * 128 + ((obytes + 1023) & ~1023)) + 2 * kStg * 8 + 1024;
+}
+
+size_t ttm_smem(int64_t dim) {
+    const int rows_pad = (int)((dim + 7) & ~7);
+    return (size_t)kStg * rows_pad * 128 + 2 * kStg * 8 + 1024;
+}
+
+template <typename KernelT>
+void set_smem(KernelT k, size_t smem) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+}  // namespace
+
+bool slab2_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right) {
+    if (dtype != F64 || left < 2 || (left & 1) || dim > 128 || K > 16 || !encode_fn()) return false;
+    if (dim * right >= (int64_t(1) << 31) || left >= (int64_t(1) << 31)) return false;  // TMA coordinates are int32
+    return sketch_smem(dim, 2) <= 220 * 1024 && ttm_smem(dim) <= 220 * 1024;
+}
+
+int64_t slab2_units(int64_t left, int64_t right) { return right * ((left + kUnitL - 1) / kUnitL); }
+
+void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
+                        int64_t rows_glob, double* out, cudaStream_t s) {
+    const int LC = (int)((left + kUnitL - 1) / kUnitL);
+    const int64_t nunits = right * LC;
+    const int NT = K <= 8 ? 1 : 2;
+    cudaMemsetAsync(out, 0, sizeof(double) * nunits * 4 * NT * 32, s);
+    const int threads = ((K * (kUnitL / 2 + 1)) + 31) & ~31;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, 148 * 12));
+    k_omega_units<<<blocks, threads, 0, s>>>(left, LC, nunits, K, NT, seed, D, col_off, rows_glob, gauss_tables(s),
+                                             out);
+}
+
+void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
+                         int num_sms, cudaStream_t s) {
+    CUtensorMap map;
+    make_map(&map, x, p.left, p.dim * p.right, p.dim);
+    Slab2Args a{};
+    a.left = p.left;
+    a.dim = p.dim;
+    a.right = p.right;
+    a.LC = (int)((p.left + kUnitL - 1) / kUnitL);
+    a.nunits = p.right * a.LC;
+    a.K = p.K;
+    a.mtiles = (int)((p.dim + 7) / 8);
+    a.partial = partial;
+    a.omega = omega_units;
+    const int NT = p.K <= 8 ? 1 : 2;
+    const size_t smem = sketch_smem(p.dim, NT);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
+    const int threads = (kTCons + 1) * 32;
+#define TRG_S2(MTW, NTV)                                                  \
+    do {                                                                  \
+        set_smem(k_slab2_sketch_f64<MTW, NTV>, smem);                     \
+        k_slab2_sketch_f64<MTW, NTV><<<grid, threads, smem, s>>>(map, a); \
+    } while (0)
+    if (a.mtiles <= 8) {
+        if (NT == 1) TRG_S2(4, 1); else TRG_S2(4, 2);
+    } else {
+        if (NT == 1) TRG_S2(8, 1); else TRG_S2(8, 2);
+    }
+#undef TRG_S2
+    launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
+}
+
+void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
+                      cudaStream_t s) {
+    CUtensorMap map;
+    make_map(&map, in, p.left, p.dim * p.right, p.dim);
+    Slab2Args a{};
+    a.left = p.left;
+    a.dim = p.dim;
+    a.right = p.right;
+    a.LC = (int)((p.left + kUnitL - 1) / kUnitL);
+    a.nunits = p.right * a.LC;
+    a.K = (int)p.odim;
+    a.Tk = 2 * (int)((p.dim + 7) / 8);  // permuted k-steps come in pairs covering 8 rows
+    a.out = reinterpret_cast<double*>(out);
+    a.q = q;
+    a.ldq = ldq;
+    const int NT = a.K <= 8 ? 1 : 2;
+    const size_t smem = ttm_smem(p.dim);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
+    const int threads = (kTCons + 1) * 32;
+#define TRG_T2(NTV, TKV)                                                  \
+    do {                                                                  \
+        set_smem(k_slab2_ttm_f64<NTV, TKV>, smem);                        \
+        k_slab2_ttm_f64<NTV, TKV><<<grid, threads, smem, s>>>(map, a);    \
+    } while (0)
+    if (a.Tk <= 16) {
+        if (NT == 1) TRG_T2(1, 16); else TRG_T2(2, 16);
+    } else if (a.Tk <= 26) {
+        if (NT == 1) TRG_T2(1, 26); else TRG_T2(2, 26);
+    } else {
+        if (NT == 1) TRG_T2(1, 32); else TRG_T2(2, 32);
+    }
+#undef TRG_T2
+}
+
+}  // namespace trg
