@@ -104,6 +104,30 @@ def kernel_bytes(cfg, label):
     return None
 
 
+def kernel_flops(cfg, label):
+    """Contraction flops of one launch: 2 * |input| * K_n (sketch or shrink of mode n)."""
+    label = label.split("+")[0]
+    dims, K = list(cfg["dims"]), list(cfg["K"])
+    cur = list(dims)
+    for n in range(len(dims)):
+        if K[n] == dims[n]:
+            continue
+        before = int(np.prod(cur))
+        if label in (f"sketch_m{n}", f"ttm_m{n}"):
+            return 2.0 * before * K[n]
+        cur[n] = K[n]
+    return None
+
+
+def fp64_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return max(v for k, v in d.items() if k.endswith("dmma"))
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -363,6 +387,14 @@ def main():
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": ncu_traffic(args.config, dom), "alg_bytes_per_launch": kb_local,
                 "avg_launch_ms": kernels[dom]["avg_ms"], "peak_source": peak_src}
+        fl = kernel_flops(cfg, dom)
+        fp64 = fp64_peak()
+        if fl and cfg["dtype"] == "f64" and fp64:
+            # the fp64 streaming kernels share the FP64 datapath (DMMA + Box-Muller DFMA): second ceiling
+            tf = fl / world / (kernels[dom]["avg_ms"] * 1e-3) / 1e12
+            roof["fp64_pipe"] = {"achieved_tflops": tf, "peak_tflops": fp64, "frac": tf / fp64,
+                                 "flops_per_launch": fl / world,
+                                 "peak_source": "measured (profiles/fp64_peak.json, DMMA m8n8k4 loop)"}
     b_alg, sizes, es = alg_bytes(cfg, args.variant)
     stage = {"alg_bytes": b_alg, "frac": b_alg / world / (ms_step * 1e-3) / 1e9 / peak,
              "definition": "SURVEY §8d B_alg / per-rank step time / measured HBM peak"}
