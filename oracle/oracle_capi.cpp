@@ -117,7 +117,7 @@ int oracle_splitmix_u64(std::uint64_t seed, std::int64_t n, std::uint64_t* out) 
 int oracle_gaussian(std::uint64_t seed, std::int64_t skip, std::int64_t n, double* out) {
     return guard([&] {
         GaussianSampler g(seed);
-        for (std::int64_t i = 0; i < skip; ++i) g.next();
+        g.seek(seed, (std::uint64_t)skip);
         for (std::int64_t i = 0; i < n; ++i) out[i] = g.next();
     });
 }

@@ -92,6 +92,15 @@ struct GaussianSampler {
         have_spare = true;
         return radius * std::cos(angle);
     }
+    // Position a fresh sampler so that the next draw is draw `d` of the stream. SplitMix64's
+    // state after k outputs is seed + k * gamma (random.hpp:18-19) and draw d comes from the
+    // uniform pair 2 floor(d/2), 2 floor(d/2) + 1 (cos for even d, sin = the cached spare for
+    // odd d), so this equals calling next() d times (pinned by the random-access tests).
+    void seek(std::uint64_t seed, std::uint64_t d) {
+        rng.state = seed + 2ull * (d >> 1) * 0x9E3779B97F4A7C15ull;
+        have_spare = false;
+        if (d & 1ull) next();  // leaves the pair's sin as the spare
+    }
 };
 
 // ---------------------------------------------------------------- containers

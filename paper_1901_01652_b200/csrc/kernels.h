@@ -54,6 +54,15 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
 bool stream_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim);
 void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                        cudaStream_t s);
+// ---- fp32 mode-0 sketch (FFMA, TMA 2-D boxes), stream_f32.cu; partial = grid_cols x dim x K
+bool stream_sketch_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
+int stream_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms, int* grid_cols);
+void launch_stream_sketch_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                              cudaStream_t s);
+bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols);
+void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
+                           cudaStream_t s);
+
 // ---- fused mode-0 shrink + mode-1 sketch (K3), fp64, left == 1
 struct FusedPlan {
     int64_t I0, I1, nfib, ldq, K0, K1;  // nfib = local mode-1 fibres = prod of local extents of modes >= 2

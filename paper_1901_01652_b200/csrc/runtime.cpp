@@ -354,6 +354,13 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_stream_sketch(p, cur, partial, ylocal, ctx->num_sms, &grid, ctx->stream);
         }, 2);
+    } else if (trg::stream_sketch_f32_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
+        int gc = 0;
+        trg::stream_sketch_f32_grid(p.dim, (int)Kn, p.right, ctx->num_sms, &gc);
+        partial = (double*)ctx->alloc(sizeof(double) * gc * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_stream_sketch_f32(p, cur, partial, ylocal, ctx->num_sms, ctx->stream);
+        }, 2);
     } else if (p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
         const int NT = Kn <= 8 ? 1 : 2;
         double* om = nullptr;
@@ -410,7 +417,11 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
     if (n == N - 1) m += x->lo;  // local rows of Q_{N-1}
     const size_t es = trg::dtype_size(x->dtype);
     void* out = ctx->alloc(es * (size_t)(p.left * Kn * p.right));
-    if (trg::stream_ttm_ok(p.dtype, p.left, p.dim, Kn)) {
+    if (trg::stream_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_stream_ttm_f32(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
+        });
+    } else if (trg::stream_ttm_ok(p.dtype, p.left, p.dim, Kn)) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
         });

@@ -29,7 +29,14 @@ namespace {
 constexpr int kStages = 3;
 constexpr int kCons = 4;    // consumer warps (shrink)
 constexpr int kSkCons = 8;  // consumer warps (sketch): 2 per SM sub-partition keep the DMMA pipe fed
-constexpr int kRng = 8;     // Omega generator warps (sketch)
+#ifndef TRG_SK_RNG
+#define TRG_SK_RNG 16
+#endif
+#ifndef TRG_SK_ILP
+#define TRG_SK_ILP 1
+#endif
+constexpr int kRng = TRG_SK_RNG;  // Omega generator warps (sketch): one Box-Muller pair per thread per tile
+constexpr int kIlp = TRG_SK_ILP;  // independent pairs per generator thread per iteration
 constexpr int kOB = 4;      // Omega tile buffers: the generators may run kOB - 1 tiles ahead
 constexpr int kPad = 8;   // zeroed doubles after each stage (A rows may overrun by < 8)
 constexpr size_t kBarBytes = 256;  // room for the mbarriers after the buffers
@@ -41,7 +48,6 @@ struct SkArgs {
     uint64_t seed, D;
     double* partial;
     const GaussTables* gt;
-    int dbg;  // TEMP experiment: 1 = skip RNG math, 2 = skip MMAs
 };
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
@@ -104,8 +110,8 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     }
     if (warp >= kSkCons) {
         // ---------------- generator warps: Omega tile in B-fragment order.
-        // Two independent Box-Muller pairs per thread per iteration (ILP 2):
-        // the fp64 log/sqrt/sincospi chains are latency-bound otherwise.
+        // kIlp independent Box-Muller pairs per thread per iteration; with 16 warps
+        // one pair per thread covers a 64 x 16 tile in a single round.
         const int rt = tid - kSkCons * 32;
         // pairs per k-column of the tile: CT/2 when every column run starts on an
         // even draw (then nothing is wasted), one more otherwise
@@ -118,13 +124,13 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             const int64_t c0 = t * CT;
             const int64_t ncol = imin64(CT, a.ncols - c0);
             double* O = omega + b * omega_elems;
-            for (int it0 = rt; it0 < nitems; it0 += 2 * kRng * 32) {
-                double z[2][2];
-                int kk[2];
-                int64_t cc[2];
-                bool live[2];
+            for (int it0 = rt; it0 < nitems; it0 += kIlp * kRng * 32) {
+                double z[kIlp][2];
+                int kk[kIlp];
+                int64_t cc[kIlp];
+                bool live[kIlp];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < kIlp; ++u) {
                     const int it = it0 + u * kRng * 32;
                     const int k = it / npmax;
                     const int jj = it - k * npmax;
@@ -133,12 +139,10 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                     live[u] = it < nitems && p <= ((s0 + (uint64_t)CT - 1ull) >> 1);
                     kk[u] = k;
                     cc[u] = (int64_t)(2ull * p - s0);
-                    z[u][0] = 0.5;
-                    z[u][1] = 0.25;
-                    if (a.dbg != 1) gauss_pair_tab(a.seed, live[u] ? p : 0ull, *tabs, z[u][0], z[u][1]);
+                    gauss_pair_tab(a.seed, live[u] ? p : 0ull, *tabs, z[u][0], z[u][1]);
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < kIlp; ++u) {
                     if (!live[u]) continue;
                     const int64_t c = cc[u];
                     if (c >= 0 && c < CT) O[omega_idx((int)c, kk[u], NT)] = c < ncol ? z[u][0] : 0.0;
@@ -169,7 +173,10 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
         mbar_wait(&full_o[b], (j / kOB) & 1);
         const double* X = stages + s * stage_elems + r * dim + q + 8 * mt0;
         const double* O = omega + b * omega_elems;
-        for (int t = tg; t < (a.dbg == 2 ? 0 : CT / 4); t += 4) {
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {  // k-steps t = tg, tg + 4, ... < CT / 4 <= 16
+            const int t = tg + 4 * i4;
+            if (t >= CT / 4) break;
             double bv[NT];
 #pragma unroll
             for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
@@ -668,7 +675,6 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.seed = p.seed;
     a.D = p.D;
     a.partial = partial;
-    a.dbg = getenv("TRG_DEBUG_SKETCH") ? atoi(getenv("TRG_DEBUG_SKETCH")) : 0;
     a.gt = gauss_tables(s);
     const int NT = nt_for(p.K);
     const int mtw = (a.mtiles + 1) / 2;  // row tiles per consumer warp (two halves)

@@ -361,3 +361,12 @@ def test_oracle_thread_count_does_not_change_results():
     orc.set_threads(max(2, orc.max_threads()))
     b = orc.sketch(x, [5, 5, 5], seed=3)[0]
     np.testing.assert_array_equal(a, b)
+
+
+def test_gaussian_seek_equals_sequential_stream():
+    # the oracle positions its sampler in O(1) (SplitMix64 state = seed + k gamma); it must
+    # equal drawing `skip` values first (random.hpp:46-71), odd skips included (cached spare)
+    for seed in (0, 3, 2**63 + 11):
+        full = orc.gaussian(seed, 2000)
+        for skip in (0, 1, 2, 7, 998, 1995):
+            np.testing.assert_array_equal(orc.gaussian(seed, 5, skip=skip), full[skip:skip + 5])
