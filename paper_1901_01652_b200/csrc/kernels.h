@@ -60,6 +60,7 @@ int stream_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms, int* 
 void launch_stream_sketch_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
                               cudaStream_t s);
 bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols);
+// writes P^(1) in fp64 (the fp32 input's later modes then run the fp64 kernels)
 void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                            cudaStream_t s);
 

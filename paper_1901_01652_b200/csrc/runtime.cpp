@@ -332,11 +332,11 @@ struct PreOmega {
     cudaEvent_t ready = nullptr;
 };
 
-void sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
-                 int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull, PreOmega* pre = nullptr) {
+void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
+                 int n, int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull, PreOmega* pre = nullptr) {
     const int N = (int)cur_shape.size();
     trg::SketchPlan p{};
-    p.dtype = x->dtype;
+    p.dtype = cdt;
     p.left = prod(cur_shape, 0, n);
     p.dim = cur_shape[n];
     p.right = prod(cur_shape, n + 1);
@@ -402,11 +402,12 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::
 }
 
 // out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
-void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std::vector<int64_t>& cur_shape, int n,
-                  int64_t Kn, const double* dQ) {
+// out = cur x_n Q^T; *odt is the output dtype (fp32 mode-0 input is promoted to fp64 by its shrink)
+void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
+                  int n, int64_t Kn, const double* dQ, int* odt) {
     const int N = (int)cur_shape.size();
     trg::TTMPlan p{};
-    p.dtype = x->dtype;
+    p.dtype = cdt;
     p.left = prod(cur_shape, 0, n);
     p.dim = cur_shape[n];
     p.right = prod(cur_shape, n + 1);
@@ -415,9 +416,11 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
     p.m_sd = 1;
     const double* m = dQ;
     if (n == N - 1) m += x->lo;  // local rows of Q_{N-1}
-    const size_t es = trg::dtype_size(x->dtype);
+    const bool promote = trg::stream_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right);
+    *odt = promote ? F64 : cdt;
+    const size_t es = trg::dtype_size(*odt);
     void* out = ctx->alloc(es * (size_t)(p.left * Kn * p.right));
-    if (trg::stream_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+    if (promote) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm_f32(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
         });
@@ -440,7 +443,7 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, const void* cur, const std:
     return out;
 }
 
-void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, const std::vector<int64_t>& K, uint64_t seed,
+void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const std::vector<int64_t>& K, uint64_t seed,
                         const std::vector<ModeOffsets>& offs, int after, std::vector<PreOmega>& pre) {
     const int N = (int)x->dims.size();
     std::vector<int64_t> shape = x->local_shape();
@@ -451,7 +454,7 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, const std::vector<int
     for (int m = after + 1; m < N; ++m) {
         if (offs[m].skipped) continue;
         const int64_t left = prod(shape, 0, m), dim = shape[m], right = prod(shape, m + 1);
-        if (left > 1 && trg::slab2_ok(x->dtype, left, dim, K[m], right)) {
+        if (left > 1 && trg::slab2_ok(later_dt, left, dim, K[m], right)) {
             const int NT = K[m] <= 8 ? 1 : 2;
             pre[m].buf = (double*)ctx->alloc(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
             CK(cudaEventRecord(go, ctx->stream));
@@ -485,7 +488,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     sk->dflags = (int*)ctx->alloc(sizeof(int) * N);
     CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * N, ctx->stream));
 
-    const size_t es = trg::dtype_size(x->dtype);
+    int cdt = x->dtype;  // dtype of the working tensor (fp32 input is promoted by its mode-0 shrink)
     std::vector<int64_t> shape = x->local_shape();
     const void* cur = x->d;
     void* owned = nullptr;  // buffer owned by the pipeline (not x)
@@ -508,14 +511,15 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
             if (!y_ready[n]) {
                 sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-                sketch_mode(ctx, x, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n]);
+                sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n]);
             }
             if (!pre_started) {
                 // Omega_m of every later slab-kernel mode depends only on shapes and the seed:
                 // generate them on the side stream while this mode's QR (one SM) and
                 // shrink (HBM-bound) run on the main stream
                 pre_started = true;
-                schedule_pre_omega(ctx, x, sk->K, seed, offs, n, pre);
+                const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
+                schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre);
             }
             qr(n);
             void* out = nullptr;
@@ -523,7 +527,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             // off by default: the separate shrink + TMA slab sketch measure faster (profiles/)
             static const bool fuse = getenv("TRG_FUSE") != nullptr;
             if (fuse && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
-                trg::fused_ttm_sketch_ok(x->dtype, 1, shape[0], Kn, shape[1], sk->K[1])) {
+                trg::fused_ttm_sketch_ok(cdt, 1, shape[0], Kn, shape[1], sk->K[1])) {
                 trg::FusedPlan fp{};
                 fp.I0 = shape[0];
                 fp.I1 = shape[1];
@@ -535,7 +539,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 fp.D1 = offs[1].D;
                 fp.rows_glob1 = offs[1].rows_glob;
                 fp.col_off1 = offs[1].col_off;
-                out = ctx->alloc(trg::dtype_size(x->dtype) * (size_t)(Kn * prod(shape, 1)));
+                out = ctx->alloc(trg::dtype_size(cdt) * (size_t)(Kn * prod(shape, 1)));
                 sk->dY[1] = (double*)ctx->alloc(sizeof(double) * x->dims[1] * sk->K[1]);
                 const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(fp.nfib, ctx->num_sms));
                 double* partial = (double*)ctx->alloc(sizeof(double) * grid * fp.I1 * fp.K1);
@@ -547,9 +551,11 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 ctx->allreduce(sk->dY[1], (size_t)(x->dims[1] * sk->K[1]), F64);
                 y_ready[1] = true;
             } else {
-                out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
+                int odt = cdt;
+                out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt);
+                cdt = odt;
             }
-            if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), x->dtype);
+            if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), cdt);
             if (owned) ctx->dfree(owned);
             owned = out;
             cur = out;
@@ -563,14 +569,16 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
             sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-            sketch_mode(ctx, x, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n]);
+            sketch_mode(ctx, x, x->dtype, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n]);
             qr(n);
         }
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
-            void* out = shrink_mode(ctx, x, cur, shape, n, Kn, sk->dQ[n]);
-            if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), x->dtype);
+            int odt = cdt;
+            void* out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt);
+            cdt = odt;
+            if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), cdt);
             if (owned) ctx->dfree(owned);
             owned = out;
             cur = out;
@@ -580,19 +588,21 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     const bool last_projected = sk->K[N - 1] != x->dims[N - 1];
     if (ctx->world > 1 && !last_projected) {
         // P still sharded along the last mode: zero-padded gather by allreduce
+        const size_t es = trg::dtype_size(cdt);
         const int64_t inner = prod(shape, 0, N - 1);
         const int64_t full = inner * x->dims[N - 1];
         void* g = ctx->alloc(es * full);
         CK(cudaMemsetAsync(g, 0, es * full, ctx->stream));
         CK(cudaMemcpyAsync((char*)g + es * inner * x->lo, cur, es * inner * (x->hi - x->lo), cudaMemcpyDeviceToDevice,
                            ctx->stream));
-        ctx->allreduce(g, (size_t)full, x->dtype);
+        ctx->allreduce(g, (size_t)full, cdt);
         if (owned) ctx->dfree(owned);
         owned = g;
         cur = g;
         shape[N - 1] = x->dims[N - 1];
     }
     sk->P_elems = prod(shape);
+    sk->dtype = cdt;  // P's dtype (fp64 once an fp32 input has been promoted)
     if (owned) {
         sk->dP = owned;
         sk->P_is_view = false;

@@ -36,13 +36,13 @@ namespace trg {
 namespace {
 
 constexpr int kF32Cons = 8;
-constexpr int kF32Gen = 4;
 constexpr int kF32Stages = 4;
 constexpr int kF32OB = 2;
 
 struct F32SkArgs {
     int64_t I0, L;          // X_(0) is I0 x L
     int DT, DTB, NB, CT;    // rows per CTA, rows per box, boxes per stage, columns per tile
+    int BS;                 // floats per box region (CT * DTB rounded up to 128 B: TMA destinations are 128-B aligned)
     int DS;                 // row splits (grid = DS x GC)
     int K, Kp, TK, nkb, ndb, G;
     int64_t ntiles;
@@ -60,14 +60,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <int TK>
-__global__ void __launch_bounds__((kF32Cons + kF32Gen + 1) * 32, 1)
+// GEN generator warps: 8 when the Omega tile is dense in draws (C5: 0.2 draws per element,
+// light consumers), 4 otherwise (C3/C4 need the registers for 4 x TK accumulators)
+template <int TK, int GEN>
+__global__ void __launch_bounds__((kF32Cons + GEN + 1) * 32, 1)
     k_sketch_l1_f32(const __grid_constant__ CUtensorMap tmap, F32SkArgs a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int kF32Gen = GEN;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int rs = blockIdx.x % a.DS;           // row split
     const int cg = blockIdx.x / a.DS;           // column CTA index
     const int GC = gridDim.x / a.DS;
-    const int stage_floats = a.NB * a.CT * a.DTB;
+    const int stage_floats = a.NB * a.BS;
     float* stages = reinterpret_cast<float*>(smem_raw);
     float* om = stages + kF32Stages * stage_floats;  // kF32OB x CT x Kp
     const int om_floats = a.CT * a.Kp;
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__((kF32Cons + kF32Gen + 1) * 32, 1)
                 const int64_t c0 = (cg + j * GC) * CT;
                 mbar_arrive_expect_tx(&full_x[s], bytes);
                 for (int b = 0; b < a.NB; ++b)
-                    tma_load_2d(stages + s * stage_floats + b * CT * a.DTB, &tmap, rs * a.DT + b * a.DTB, (int)c0,
+                    tma_load_2d(stages + s * stage_floats + b * a.BS, &tmap, rs * a.DT + b * a.DTB, (int)c0,
                                 &full_x[s], pol);
             }
         }
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__((kF32Cons + kF32Gen + 1) * 32, 1)
         mbar_wait(&full_x[s], (uint32_t)((j / kF32Stages) & 1));
         mbar_wait(&full_o[b], (uint32_t)((j / kF32OB) & 1));
         if (active) {
-            const float* X = stages + s * stage_floats + box * CT * a.DTB + rin;
+            const float* X = stages + s * stage_floats + box * a.BS + rin;
             const float* O = om + b * om_floats + k0;
 #pragma unroll 1
             for (int c = g; c < CT; c += a.G) {
@@ -235,7 +238,7 @@ struct F32TtArgs {
     int64_t I0, L;  // X_(0) is I0 x L (fibres of I0)
     int DC, NCH, K, Kp;
     int64_t nunits;  // ceil(L / 64)
-    float* out;      // P^(1): row m, K outputs (first-index-fastest: o fastest)
+    double* out;     // P^(1) promoted to fp64: row m, K outputs (o fastest); later modes run fp64
 };
 
 template <int KP>
@@ -333,10 +336,10 @@ __global__ void __launch_bounds__((kTtCons + 1) * 32, 1)
         for (int f = 0; f < 2; ++f) {
             const int64_t m = u * 64 + lane + 32 * f;
             if (m >= a.L) continue;
-            float* dst = a.out + m * a.K;
+            double* dst = a.out + m * a.K;
 #pragma unroll
             for (int o = 0; o < KP; ++o)
-                if (o < a.K) dst[o] = acc[f][o];
+                if (o < a.K) dst[o] = (double)acc[f][o];
         }
     }
 }
@@ -355,7 +358,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 struct F32Plan {
-    int DS, DT, DTB, NB, CT, TK, nkb, ndb, G, Kp;
+    int DS, DT, DTB, NB, CT, BS, TK, nkb, ndb, G, Kp;
     size_t smem;
 };
 
@@ -386,9 +389,10 @@ bool plan_f32(int64_t I0, int K, F32Plan& p) {
         p.G = (kF32Cons * 32) / (ndb * p.nkb);
         // ~32 KB stages, at most 256 columns per box
         p.CT = std::max(4, std::min(256, (int)(32768 / (4 * p.NB * p.DTB)) & ~3));
-        p.smem = (size_t)kF32Stages * p.NB * p.CT * p.DTB * 4 + (size_t)kF32OB * p.CT * p.Kp * 4 + 256;
+        p.BS = (p.CT * p.DTB + 31) & ~31;
+        p.smem = (size_t)kF32Stages * p.NB * p.BS * 4 + (size_t)kF32OB * p.CT * p.Kp * 4 + 256;
         const size_t red = p.G > 1 ? (size_t)p.DT * p.Kp * 8 : 0;  // G > 1: group reduction scratch
-        if (red > (size_t)kF32Stages * p.NB * p.CT * p.DTB * 4) p.smem += red;
+        if (red > (size_t)kF32Stages * p.NB * p.BS * 4) p.smem += red;
         return p.smem <= 220 * 1024;
     }
     return false;
@@ -421,6 +425,7 @@ void launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* parti
     a.DTB = p.DTB;
     a.NB = p.NB;
     a.CT = p.CT;
+    a.BS = p.BS;
     a.DS = p.DS;
     a.K = sp.K;
     a.Kp = p.Kp;
@@ -445,11 +450,11 @@ void launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* parti
     int gc = 0;
     const int grid = stream_sketch_f32_grid(sp.dim, sp.K, sp.right, num_sms, &gc);
     cudaMemsetAsync(partial, 0, sizeof(double) * gc * sp.dim * sp.K, s);
-    const int threads = (kF32Cons + kF32Gen + 1) * 32;
-#define TRG_F32(TKV)                                                                                      \
-    do {                                                                                                  \
-        cudaFuncSetAttribute(k_sketch_l1_f32<TKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem); \
-        k_sketch_l1_f32<TKV><<<grid, threads, p.smem, s>>>(map, a);                                       \
+#define TRG_F32(TKV)                                                                                          \
+    do {                                                                                                      \
+        constexpr int G = TKV <= 12 ? 8 : 4;                                                                  \
+        cudaFuncSetAttribute(k_sketch_l1_f32<TKV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem); \
+        k_sketch_l1_f32<TKV, G><<<grid, (kF32Cons + G + 1) * 32, p.smem, s>>>(map, a);                        \
     } while (0)
     switch (p.TK) {
         case 4: TRG_F32(4); break;
@@ -483,7 +488,7 @@ void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const do
     a.K = (int)p.odim;
     a.Kp = (int)((p.odim + 3) & ~3);
     a.nunits = (p.right + 63) / 64;
-    a.out = reinterpret_cast<float*>(out);
+    a.out = reinterpret_cast<double*>(out);
     CUtensorMap map;
     const cuuint64_t gdim[2] = {(cuuint64_t)p.dim, (cuuint64_t)p.right};
     const cuuint64_t gstride[1] = {(cuuint64_t)p.dim * 4};
