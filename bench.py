@@ -253,15 +253,8 @@ def cpu_baseline(cfg, budget_s=20.0, steps=1):
 
 def reference_arm(args, cfg):
     rank, world, _ = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("gloo")
-        if rank != 0:
-            dist.barrier()
-            return
-    for _ in range(args.warmup and 1):
-        pass
+    if rank != 0:
+        return  # under torchrun only rank 0 times the CPU reference; the others exit 0 without work
     budget = 120.0
     orc, shape, run = cpu_sample(cfg, budget, args.steps + args.warmup)
     threads = os.cpu_count() or 1
@@ -284,10 +277,6 @@ def reference_arm(args, cfg):
                              "sample": f"oracle sketch() of a {'x'.join(map(str, shape))} sample per step"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
 
 
 # ------------------------------------------------------------------ GPU arm

@@ -39,7 +39,7 @@ struct TTMPlan {
     int64_t left, dim, right, odim;
     int64_t m_so, m_sd;
     // derived
-    int TM, TO, MT, DT, nm, no, OT, threads, noT;
+    int TM, TO, MT, DT, nm, no, OT, threads, noT, dsplit;
     int64_t rows, nrowtiles;
     int grid_x;
     size_t smem;

@@ -26,6 +26,8 @@ struct TTMArgs {
     int64_t left, dim, odim, rows, m_so, m_sd, nrowtiles;
     int MT, DT, nm, no, OT;
     FastDiv left_div;
+    int64_t dlen;   // contraction range per grid.z slice (split-d for few row tiles)
+    double* part;   // split-d: fp64 partial outputs [gridDim.z][rows * odim] in the output layout
 };
 
 template <typename T, int TM, int TO, bool LEFT1>
@@ -53,7 +55,9 @@ __global__ void __launch_bounds__(256) k_ttm(TTMArgs a) {
 #pragma unroll
             for (int j = 0; j < TO; ++j) acc[i][j] = A(0);
 
-        for (int64_t d0 = 0; d0 < a.dim; d0 += DT) {
+        const int64_t d_lo = (int64_t)blockIdx.z * a.dlen;
+        const int64_t d_hi = d_lo + a.dlen < a.dim ? d_lo + a.dlen : a.dim;
+        for (int64_t d0 = d_lo; d0 < d_hi; d0 += DT) {
             __syncthreads();
             if (LEFT1) {
                 // rows are contiguous runs of dim elements: threads sweep d fastest
@@ -62,7 +66,7 @@ __global__ void __launch_bounds__(256) k_ttm(TTMArgs a) {
                     const int dd = e - mm * DT;
                     const int64_t m = m0 + mm, d = d0 + dd;
                     T v = T(0);
-                    if (m < a.rows && d < a.dim) v = __ldcs(in + d + a.dim * m);
+                    if (m < a.rows && d < d_hi) v = __ldcs(in + d + a.dim * m);
                     Xs[dd * MTp + mm] = v;
                 }
             } else {
@@ -72,7 +76,7 @@ __global__ void __launch_bounds__(256) k_ttm(TTMArgs a) {
                     const int mm = e - dd * MT;
                     const int64_t m = m0 + mm, d = d0 + dd;
                     T v = T(0);
-                    if (m < a.rows && d < a.dim) {
+                    if (m < a.rows && d < d_hi) {
                         const uint32_t r = a.left_div.div((uint32_t)m);
                         const int64_t l = m - (int64_t)r * a.left;
                         v = __ldcs(in + l + a.left * (d + a.dim * (int64_t)r));
@@ -84,10 +88,10 @@ __global__ void __launch_bounds__(256) k_ttm(TTMArgs a) {
                 const int dd = e / OT;
                 const int oo = e - dd * OT;
                 const int64_t d = d0 + dd, o = o0 + oo;
-                Ms[dd * OT + oo] = (d < a.dim && o < a.odim) ? T(a.m[o * a.m_so + d * a.m_sd]) : T(0);
+                Ms[dd * OT + oo] = (d < d_hi && o < a.odim) ? T(a.m[o * a.m_so + d * a.m_sd]) : T(0);
             }
             __syncthreads();
-            const int dlim = (a.dim - d0) < DT ? (int)(a.dim - d0) : DT;
+            const int dlim = (d_hi - d0) < DT ? (int)(d_hi - d0) : DT;
             for (int dd = 0; dd < dlim; ++dd) {
                 T xv[TM], mv[TO];
 #pragma unroll
@@ -105,21 +109,29 @@ __global__ void __launch_bounds__(256) k_ttm(TTMArgs a) {
         for (int i = 0; i < TM; ++i) {
             const int64_t m = m0 + mg + a.nm * i;
             if (m >= a.rows) continue;
+            int64_t base, ostride;  // output layout: out(l, o, r) at l + left*(o + odim*r)
             if (LEFT1) {
-                T* dst = out + a.odim * m;
-#pragma unroll
-                for (int j = 0; j < TO; ++j) {
-                    const int64_t o = o0 + og * TO + j;
-                    if (o < a.odim) dst[o] = T(acc[i][j]);
-                }
+                base = a.odim * m;
+                ostride = 1;
             } else {
                 const uint32_t r = a.left_div.div((uint32_t)m);
                 const int64_t l = m - (int64_t)r * a.left;
-                T* dst = out + l + a.left * a.odim * (int64_t)r;
+                base = l + a.left * a.odim * (int64_t)r;
+                ostride = a.left;
+            }
+            if (a.part) {
+                double* dst = a.part + (int64_t)blockIdx.z * a.rows * a.odim + base;
 #pragma unroll
                 for (int j = 0; j < TO; ++j) {
                     const int64_t o = o0 + og * TO + j;
-                    if (o < a.odim) dst[a.left * o] = T(acc[i][j]);
+                    if (o < a.odim) dst[ostride * o] = (double)acc[i][j];
+                }
+            } else {
+                T* dst = out + base;
+#pragma unroll
+                for (int j = 0; j < TO; ++j) {
+                    const int64_t o = o0 + og * TO + j;
+                    if (o < a.odim) dst[ostride * o] = T(acc[i][j]);
                 }
             }
         }
@@ -133,7 +145,7 @@ void run(const TTMPlan& p, const TTMArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(k_ttm<T, TM, TO, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
         done = p.smem;
     }
-    dim3 grid(p.grid_x, p.noT);
+    dim3 grid(p.grid_x, p.noT, p.dsplit);
     k_ttm<T, TM, TO, L1><<<grid, p.threads, p.smem, s>>>(a);
 }
 
@@ -169,6 +181,13 @@ void plan_ttm(TTMPlan& p, int num_sms) {
     const int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / p.smem)));
     const int64_t want = (int64_t)num_sms * per_sm / std::max(1, p.noT);
     p.grid_x = (int)std::max<int64_t>(1, std::min<int64_t>(p.nrowtiles, want));
+    // few row tiles and a long contraction: split d over grid.z (fp64 partials, fixed-order sum)
+    p.dsplit = 1;
+    const int64_t ctas = (int64_t)p.grid_x * p.noT;
+    if (ctas < num_sms && p.dim >= 256) {
+        const int64_t byd = std::max<int64_t>(1, p.dim / 128);
+        p.dsplit = (int)std::max<int64_t>(1, std::min<int64_t>(byd, (2 * (int64_t)num_sms + ctas - 1) / ctas));
+    }
 }
 
 void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cudaStream_t s) {
@@ -189,12 +208,28 @@ void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cu
     a.no = p.no;
     a.OT = p.OT;
     a.left_div = FastDiv((uint32_t)std::max<int64_t>(1, std::min<int64_t>(p.left, 0xFFFFFFFFll)));
+    a.dlen = ((p.dim + p.dsplit - 1) / p.dsplit + 31) / 32 * 32;
+    a.part = nullptr;
+    const int64_t nout = p.rows * p.odim;
+    if (p.dsplit > 1) cudaMallocAsync(&a.part, sizeof(double) * nout * p.dsplit, s);
     if (p.dtype == F64) {
         if (p.TO == 8) run_l<double, 4, 8>(p, a, s);
         else run_l<double, 4, 4>(p, a, s);
     } else {
         if (p.TO == 8) run_l<float, 4, 8>(p, a, s);
         else run_l<float, 4, 4>(p, a, s);
+    }
+    if (p.dsplit > 1) {  // fixed-order sum of the d-slices (bit-reproducible)
+        if (p.dtype == F64) {
+            launch_reduce_partials(a.part, p.dsplit, nout, reinterpret_cast<double*>(out), s);
+        } else {
+            double* tmp = nullptr;
+            cudaMallocAsync(&tmp, sizeof(double) * nout, s);
+            launch_reduce_partials(a.part, p.dsplit, nout, tmp, s);
+            launch_convert(tmp, F64, out, F32, nout, s);
+            cudaFreeAsync(tmp, s);
+        }
+        cudaFreeAsync(a.part, s);
     }
 }
 
