@@ -250,6 +250,7 @@ class DeviceSketch:
 
     def __init__(self, ctx, x, spec, variant=L.TRG_SEQUENTIAL):
         self.ctx = ctx
+        self._x = x  # the projection may be recomputed from x when first read (deferred mode)
         self.dims = list(x.shape)
         self.K = [int(k) for k in spec.sketch_dims]
         self._h = ctypes.c_void_p()

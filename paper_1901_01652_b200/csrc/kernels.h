@@ -88,6 +88,8 @@ int64_t slab2_units(int64_t left, int64_t right);
 // unit blocks of the reference test matrix (4 x NT x 32 doubles per unit), L2-resident
 void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
                         int64_t rows_glob, double* out, cudaStream_t s);
+// standard-layout test matrix (rows left*right, K columns) -> unit blocks
+void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s);
 void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
                          int num_sms, cudaStream_t s);
 void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
@@ -98,6 +100,8 @@ void launch_reduce_partials(const double* partial, int nblocks, int64_t n, doubl
 // ---- thin QR with diag(R) >= 0 (K4): CholQR2 + Householder fallback, fp64.
 // Y is m x k column-major; Q (m x k) out. work >= m*k doubles + 2*k.
 void launch_qr(const double* y, int64_t m, int k, double* q, double* work, int* flag, cudaStream_t s);
+// Rinv = (upper(Q^T Y))^-1, k x k col-major, so that Q = Y Rinv; *bad set if R is near-singular
+void launch_rinv(const double* q, const double* y, int64_t m, int k, double* rinv, int* bad, cudaStream_t s);
 
 // ---- per-device tables of the table-driven Box-Muller (common.cuh), built on first use
 struct GaussTables;

@@ -230,17 +230,26 @@ struct trg_sketch {
     std::vector<int64_t> dims, K;
     std::vector<double*> dQ;  // device Q_n (nullptr for skipped modes)
     std::vector<double*> dY;  // device Y_n full rows
-    int* dflags = nullptr;
+    int* dflags = nullptr;    // N QR-path flags, then (deferred) N near-singular-R flags
     void* dP = nullptr;       // device P (dtype), full prod K
     bool P_is_view = false;   // P aliases x (no mode projected, unsharded)
     int64_t P_elems = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // deferred projection (run_sketch_deferred): validated lazily when results are read
+    const trg_tensor* x = nullptr;
+    uint64_t seed = 0;
+    bool deferred = false, checked = true;
+    void release() {
+        for (double*& p : dQ) ctx->dfree(p), p = nullptr;
+        for (double*& p : dY) ctx->dfree(p), p = nullptr;
+        ctx->dfree(dflags);
+        dflags = nullptr;
+        if (!P_is_view) ctx->dfree(dP);
+        dP = nullptr;
+    }
     ~trg_sketch() {
         if (!ctx) return;
-        for (double* p : dQ) ctx->dfree(p);
-        for (double* p : dY) ctx->dfree(p);
-        ctx->dfree(dflags);
-        if (!P_is_view) ctx->dfree(dP);
+        release();
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -471,7 +480,160 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const s
     CK(cudaEventDestroy(go));
 }
 
-void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk) {
+// ------------------------------------------------------------------ deferred projection
+// Q_n = Y_n Rinv_n for any QR with invertible R (here Rinv = upper(Q_n^T Y_n)^-1), so
+//   P^(n+1) = P^(n) x_n Q_n^T = (P^(n) x_n Y_n^T) x_n Rinv_n^T,
+// and mode products on different modes commute. The shrink of mode n can therefore start as
+// soon as Y_n is reduced, with Y_n in place of Q_n, while the QR of Y_n (a one-SM,
+// latency-bound kernel) runs on the side stream; the deferred factors are folded into
+//   * the next modes' test matrices: with Ptilde = X x_m Y_m^T (m < n), the mode-n sketch
+//     P^(n)_(n) Omega_n equals Ptilde_(n) Omegatilde_n, Omegatilde_n = Omega_n x_0 Rinv_0
+//     x_1 Rinv_1 ... (a small transform of the L2-resident test matrix, side stream), and
+//   * the final P = Ptilde x_0 Rinv_0^T x_1 ... (tiny).
+// Mathematically this is the reference's sequential projection (sketch.hpp:62-89) with the
+// same Omega draws; only the association order of the products changes. If any QR takes the
+// Householder path or R is near-singular, the result is recomputed eagerly when it is read.
+// Opt-in (TRG_DEFERRED=1): measured slower on C2 so far (profiles/README.md): the persistent
+// one-CTA-per-SM streaming kernels leave no room for the side stream's QR / transform
+// kernels, so the side pipeline serialises behind them instead of overlapping.
+bool deferred_eligible(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, int variant) {
+    static const bool on = getenv("TRG_DEFERRED") != nullptr;
+    if (!on || ctx->world != 1 || variant != TRG_SEQUENTIAL) return false;
+    const int N = (int)x->dims.size();
+    std::vector<int64_t> shape = x->local_shape();
+    int cdt = x->dtype;
+    bool first = true;
+    for (int n = 0; n < N; ++n) {
+        if (K[n] == x->dims[n]) continue;
+        const int64_t left = prod(shape, 0, n), dim = shape[n], right = prod(shape, n + 1);
+        if (first) {
+            if (trg::stream_ttm_f32_ok(cdt, left, dim, K[n], right)) cdt = F64;
+            first = false;
+        } else if (!(left > 1 && trg::slab2_ok(cdt, left, dim, K[n], right))) {
+            return false;  // later modes must take their test matrix from memory (slab kernels)
+        }
+        shape[n] = K[n];
+    }
+    return !first;
+}
+
+void run_sketch_deferred(trg_ctx* ctx, const trg_tensor* x, uint64_t seed, trg_sketch* sk) {
+    const int N = (int)x->dims.size();
+    const std::vector<int64_t>& K = sk->K;
+    const std::vector<ModeOffsets> offs = sketch_offsets(x->dims, K.data(), x->lo, TRG_SEQUENTIAL);
+    std::vector<int> proj;
+    for (int n = 0; n < N; ++n)
+        if (K[n] != x->dims[n]) proj.push_back(n);
+    std::vector<int64_t> shape = x->local_shape();
+    int cdt = x->dtype;
+    const void* cur = x->d;
+    void* owned = nullptr;
+    std::vector<double*> rinv(N, nullptr);
+    std::vector<cudaEvent_t> ev_y(N, nullptr), ev_r(N, nullptr);
+    std::vector<PreOmega> pre(N);
+    auto mk_event = [&]() {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return e;
+    };
+    auto side_alloc = [&](size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, bytes ? bytes : 8, ctx->side));
+        return p;
+    };
+    for (size_t idx = 0; idx < proj.size(); ++idx) {
+        const int n = proj[idx];
+        const int64_t In = x->dims[n], Kn = K[n];
+        sk->dY[n] = (double*)ctx->alloc(sizeof(double) * In * Kn);
+        sk->dQ[n] = (double*)ctx->alloc(sizeof(double) * In * Kn);
+        rinv[n] = (double*)ctx->alloc(sizeof(double) * Kn * Kn);
+        sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], idx ? &pre[n] : nullptr);
+        ev_y[n] = mk_event();
+        CK(cudaEventRecord(ev_y[n], ctx->stream));
+        // ---- side stream: QR of Y_n, Rinv_n, and the next mode's transformed test matrix
+        CK(cudaStreamWaitEvent(ctx->side, ev_y[n], 0));
+        double* work = (double*)side_alloc(sizeof(double) * In * Kn);
+        trg::launch_qr(sk->dY[n], In, (int)Kn, sk->dQ[n], work, sk->dflags + n, ctx->side);
+        CK(cudaFreeAsync(work, ctx->side));
+        trg::launch_rinv(sk->dQ[n], sk->dY[n], In, (int)Kn, rinv[n], sk->dflags + N + n, ctx->side);
+        ctx->launches += 2;
+        ev_r[n] = mk_event();
+        CK(cudaEventRecord(ev_r[n], ctx->side));
+        if (idx + 1 < proj.size()) {
+            const int m = proj[idx + 1];
+            std::vector<int64_t> sm = shape;  // the working shape at mode m
+            sm[n] = Kn;
+            const int64_t left = prod(sm, 0, m), right = prod(sm, m + 1), Km = K[m];
+            const int64_t rows = left * right;
+            double* om = (double*)side_alloc(sizeof(double) * rows * Km);
+            trg::launch_omega(seed, offs[m].D, offs[m].rows_glob, Km, om, ctx->side);  // rows_glob == rows here
+            // Omegatilde = Omega x_j Rinv_j for every earlier projected mode j, on the view
+            // (sm[0], ..., sm[m-1], right * K_m)
+            for (size_t jj = 0; jj <= idx; ++jj) {
+                const int j = proj[jj];
+                trg::TTMPlan tp{};
+                tp.dtype = F64;
+                tp.left = prod(sm, 0, j);
+                tp.dim = K[j];
+                tp.right = prod(sm, j + 1, m) * right * Km;
+                tp.odim = K[j];
+                tp.m_so = 1;  // M(o, d) = Rinv_j[o + K_j d]
+                tp.m_sd = K[j];
+                trg::plan_ttm(tp, ctx->num_sms);
+                double* o2 = (double*)side_alloc(sizeof(double) * rows * Km);
+                trg::launch_ttm(tp, om, o2, rinv[j], ctx->side);
+                CK(cudaFreeAsync(om, ctx->side));
+                om = o2;
+            }
+            const int NT = Km <= 8 ? 1 : 2;
+            pre[m].buf = (double*)side_alloc(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
+            trg::launch_pack_units(om, left, right, (int)Km, pre[m].buf, ctx->side);
+            CK(cudaFreeAsync(om, ctx->side));
+            ctx->launches += 3 + (int64_t)idx + 1;
+            pre[m].ready = mk_event();
+            CK(cudaEventRecord(pre[m].ready, ctx->side));
+        }
+        // ---- main stream: shrink with Y_n in place of Q_n
+        int odt = cdt;
+        void* out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dY[n], &odt);
+        if (owned) ctx->dfree(owned);
+        owned = out;
+        cur = out;
+        cdt = odt;
+        shape[n] = Kn;
+    }
+    // ---- fold the deferred factors into P: P = Ptilde x_j Rinv_j^T
+    for (int n : proj) {
+        CK(cudaStreamWaitEvent(ctx->stream, ev_r[n], 0));
+        trg::TTMPlan tp{};
+        tp.dtype = cdt;
+        tp.left = prod(shape, 0, n);
+        tp.dim = K[n];
+        tp.right = prod(shape, n + 1);
+        tp.odim = K[n];
+        tp.m_so = K[n];  // M(o, d) = Rinv_n^T(o, d) = Rinv_n[d + K_n o]
+        tp.m_sd = 1;
+        trg::plan_ttm(tp, ctx->num_sms);
+        void* o2 = ctx->alloc(trg::dtype_size(cdt) * (size_t)prod(shape));
+        ctx->launch("rinv_fold", [&] { trg::launch_ttm(tp, cur, o2, rinv[n], ctx->stream); });
+        ctx->dfree(owned);
+        owned = o2;
+        cur = o2;
+    }
+    for (int n : proj) {
+        ctx->dfree(rinv[n]);
+        cudaEventDestroy(ev_y[n]);
+        cudaEventDestroy(ev_r[n]);
+        if (pre[n].ready) cudaEventDestroy(pre[n].ready);
+    }
+    sk->P_elems = prod(shape);
+    sk->dtype = cdt;
+    sk->dP = owned;
+    sk->P_is_view = false;
+}
+
+void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk,
+                bool allow_deferred = true) {
     const int N = (int)x->dims.size();
     validate_K(x, Kin);
     require(variant == TRG_SEQUENTIAL || variant == TRG_FUSED, "sketch: unknown variant");
@@ -482,11 +644,22 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     sk->K.assign(Kin, Kin + N);
     sk->dQ.assign(N, nullptr);
     sk->dY.assign(N, nullptr);
-    CK(cudaEventCreate(&sk->ev0));
-    CK(cudaEventCreate(&sk->ev1));
+    if (!sk->ev0) CK(cudaEventCreate(&sk->ev0));
+    if (!sk->ev1) CK(cudaEventCreate(&sk->ev1));
     CK(cudaEventRecord(sk->ev0, ctx->stream));
-    sk->dflags = (int*)ctx->alloc(sizeof(int) * N);
-    CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * N, ctx->stream));
+    sk->dflags = (int*)ctx->alloc(sizeof(int) * 2 * N);
+    CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 2 * N, ctx->stream));
+    sk->x = x;
+    sk->seed = seed;
+    if (allow_deferred && deferred_eligible(ctx, x, Kin, variant)) {
+        sk->deferred = true;
+        sk->checked = false;
+        run_sketch_deferred(ctx, x, seed, sk);
+        CK(cudaEventRecord(sk->ev1, ctx->stream));
+        return;
+    }
+    sk->deferred = false;
+    sk->checked = true;
 
     int cdt = x->dtype;  // dtype of the working tensor (fp32 input is promoted by its mode-0 shrink)
     std::vector<int64_t> shape = x->local_shape();
@@ -617,7 +790,30 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     CK(cudaEventRecord(sk->ev1, ctx->stream));
 }
 
+// Deferred projections are checked when first read: a Householder-path QR or a near-singular
+// R invalidates the Y-for-Q substitution, and the projection is then recomputed eagerly.
+void validate(const trg_sketch* csk) {
+    trg_sketch* sk = const_cast<trg_sketch*>(csk);
+    if (!sk->deferred || sk->checked) return;
+    const int N = (int)sk->dims.size();
+    std::vector<int> f(2 * N);
+    CK(cudaMemcpyAsync(f.data(), sk->dflags, sizeof(int) * 2 * N, cudaMemcpyDeviceToHost, sk->ctx->stream));
+    CK(cudaStreamSynchronize(sk->ctx->stream));
+    sk->checked = true;
+    bool bad = false;
+    for (int v : f) bad = bad || v != 0;
+    if (!bad) return;
+    trg_ctx* ctx = sk->ctx;
+    const trg_tensor* x = sk->x;
+    const std::vector<int64_t> K = sk->K;
+    const uint64_t seed = sk->seed;
+    sk->release();
+    run_sketch(ctx, x, K.data(), seed, TRG_SEQUENTIAL, sk, /*allow_deferred=*/false);
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+
 void download_P(const trg_sketch* sk, std::vector<double>& out) {
+    validate(sk);
     trg_ctx* ctx = sk->ctx;
     out.resize((size_t)sk->P_elems);
     if (sk->dtype == F64) {
@@ -632,6 +828,7 @@ void download_P(const trg_sketch* sk, std::vector<double>& out) {
 }
 
 void download_basis(const trg_sketch* sk, int n, double* out) {
+    validate(sk);
     const int64_t In = sk->dims[n], Kn = sk->K[n];
     if (!sk->dQ[n]) {
         for (int64_t j = 0; j < Kn; ++j)
@@ -1143,6 +1340,7 @@ int trg_sketch_basis(const trg_sketch* sk, int mode, double* out) {
 
 int trg_sketch_y(const trg_sketch* sk, int mode, double* out) {
     return guard([&] {
+        validate(sk);
         if (mode < 0 || mode >= (int)sk->dims.size())
             throw std::out_of_range("DenseTensor: mode " + std::to_string(mode) + " out of range");
         const int64_t n = sk->dims[mode] * sk->K[mode];
@@ -1157,6 +1355,7 @@ int trg_sketch_y(const trg_sketch* sk, int mode, double* out) {
 
 int trg_sketch_qr_path(const trg_sketch* sk, int mode, int* hh) {
     return guard([&] {
+        validate(sk);
         if (mode < 0 || mode >= (int)sk->dims.size()) throw std::out_of_range("mode out of range");
         int v = 0;
         CK(cudaMemcpyAsync(&v, sk->dflags + mode, sizeof(int), cudaMemcpyDeviceToHost, sk->ctx->stream));

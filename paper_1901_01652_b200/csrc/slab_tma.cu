@@ -40,7 +40,7 @@ namespace trg {
 namespace {
 
 constexpr int kTCons = 8;    // consumer warps: pairs (w, w + 4) share a unit, two per SM sub-partition
-constexpr int kStg = 8;      // stages (units in flight)
+constexpr int kMaxStg = 8;  // stages (units in flight): 8 measured best (16 was slower on C2/C5 mode 1)
 constexpr int kUnitL = 16;   // left-chunk width of a unit (16 doubles = 128 B rows)
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
@@ -59,7 +59,7 @@ struct Slab2Args {
     int64_t left, dim, right;  // local view
     int LC;                    // ceil(left / 16) chunks per slab index
     int64_t nunits;            // right * LC
-    int K, mtiles, Tk;
+    int K, mtiles, Tk, S;  // S = stages
     double* partial;           // sketch: per-CTA Y partial (dim x K)
     const double* omega;       // sketch: unit blocks of 4 x NT x 32 doubles
     double* out;               // ttm
@@ -113,14 +113,17 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     const int sbytes = xbytes + ((obytes + 1023) & ~1023);
     // dynamic smem is only guaranteed 16-B aligned: align the ring to 1024 B by hand
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int kStg = a.S;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStg * sbytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + kStg;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nl = (a.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    // rows dim..rows_pad-1 are never written by TMA: zero them once (their products land in
-    // accumulator rows that are dropped, but must stay finite)
-    for (int i = tid; i < kStg * sbytes / 8; i += blockDim.x) reinterpret_cast<double*>(base)[i] = 0.0;
+    {  // rows dim..rows_pad-1 of every stage are never written by TMA: zero them once
+        const int npad = (rows_pad - dim) * 16;
+        for (int i = tid; i < kStg * npad; i += blockDim.x)
+            reinterpret_cast<double*>(base + (i / npad) * sbytes)[dim * 16 + i % npad] = 0.0;
+    }
     if (tid == 0) {
         for (int s = 0; s < kStg; ++s) {
             mbar_init(&full[s], 1);
@@ -218,13 +221,18 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     const int rows_pad = (dim + 7) & ~7;
     const int sbytes = rows_pad * 128;
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int kStg = a.S;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStg * sbytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + kStg;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nl = (a.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int q = lane >> 2, rl = lane & 3;
-    for (int i = tid; i < kStg * sbytes / 8; i += blockDim.x) reinterpret_cast<double*>(base)[i] = 0.0;
+    {  // rows dim..rows_pad-1 of every stage are never written by TMA: zero them once
+        const int npad = (rows_pad - dim) * 16;
+        for (int i = tid; i < kStg * npad; i += blockDim.x)
+            reinterpret_cast<double*>(base + (i / npad) * sbytes)[dim * 16 + i % npad] = 0.0;
+    }
     // B fragments of Q in registers: qb[t][jn] = Q(d = perm_d(t, rl), o = 8 jn + q)
     double qb[TKM][NT];
 #pragma unroll
@@ -295,6 +303,25 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     }
 }
 
+
+// Re-block a test matrix given in the standard layout (rows c = l + left r, K columns,
+// column-major) into the unit blocks consumed by k_slab2_sketch_f64 (the deferred projection
+// transforms Omega_n in the standard layout first).
+__global__ void k_pack_units(const double* __restrict__ om, int64_t rows, int64_t left, int LC, int64_t nunits, int K,
+                             int NT, double* out) {
+    const int64_t per = 4 * NT * 32;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nunits * per; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = e / per;
+        const int w = (int)(e - u * per);
+        const int lane = w & 31, jn = (w >> 5) % NT, t = (w >> 5) / NT;
+        const int64_t r = u / LC;
+        const int lc = (int)(u - r * LC);
+        const int64_t l = (int64_t)kUnitL * lc + 4 * t + (lane & 3);
+        const int k = 8 * jn + (lane >> 2);
+        out[e] = (l < left && k < K) ? om[(l + left * r) + rows * k] : 0.0;
+    }
+}
+
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static std::once_flag once;
@@ -322,16 +349,18 @@ bool make_map(CUtensorMap* m, const void* x, int64_t left, int64_t rows, int64_t
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-size_t sketch_smem(int64_t dim, int NT) {
+size_t sketch_stage(int64_t dim, int NT) {
     const int rows_pad = (int)((dim + 7) & ~7);
     const int obytes = 4 * NT * 32 * 8;
-    return (size_t)kStg * (rows_pad * 128 + ((obytes + 1023) & ~1023)) + 2 * kStg * 8 + 1024;
+    return (size_t)(rows_pad * 128 + ((obytes + 1023) & ~1023));
 }
-
-size_t ttm_smem(int64_t dim) {
-    const int rows_pad = (int)((dim + 7) & ~7);
-    return (size_t)kStg * rows_pad * 128 + 2 * kStg * 8 + 1024;
+size_t ttm_stage(int64_t dim) { return (size_t)((dim + 7) & ~7) * 128; }
+constexpr size_t kSlabBudget = 220 * 1024;
+int stages_for(size_t stage) {  // >= 4 (one per warp pair); as many as fit up to kMaxStg
+    int S = (int)((kSlabBudget - 1024 - 2 * kMaxStg * 8) / stage);
+    return std::min(kMaxStg, S);
 }
+size_t slab_smem(size_t stage, int S) { return (size_t)S * stage + 2 * S * 8 + 1024; }
 
 template <typename KernelT>
 void set_smem(KernelT k, size_t smem) {
@@ -343,7 +372,7 @@ void set_smem(KernelT k, size_t smem) {
 bool slab2_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right) {
     if (dtype != F64 || left < 2 || (left & 1) || dim > 128 || K > 16 || !encode_fn()) return false;
     if (dim * right >= (int64_t(1) << 31) || left >= (int64_t(1) << 31)) return false;  // TMA coordinates are int32
-    return sketch_smem(dim, 2) <= 220 * 1024 && ttm_smem(dim) <= 220 * 1024;
+    return stages_for(sketch_stage(dim, 2)) >= 4 && stages_for(ttm_stage(dim)) >= 4;
 }
 
 int64_t slab2_units(int64_t left, int64_t right) { return right * ((left + kUnitL - 1) / kUnitL); }
@@ -358,6 +387,15 @@ void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint6
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, 148 * 12));
     k_omega_units<<<blocks, threads, 0, s>>>(left, LC, nunits, K, NT, seed, D, col_off, rows_glob, gauss_tables(s),
                                              out);
+}
+
+void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s) {
+    const int LC = (int)((left + kUnitL - 1) / kUnitL);
+    const int64_t nunits = right * LC;
+    const int NT = K <= 8 ? 1 : 2;
+    const int64_t n = nunits * 4 * NT * 32;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_pack_units<<<blocks, 256, 0, s>>>(om, left * right, left, LC, nunits, K, NT, out);
 }
 
 void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
@@ -375,7 +413,8 @@ void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega
     a.partial = partial;
     a.omega = omega_units;
     const int NT = p.K <= 8 ? 1 : 2;
-    const size_t smem = sketch_smem(p.dim, NT);
+    a.S = stages_for(sketch_stage(p.dim, NT));
+    const size_t smem = slab_smem(sketch_stage(p.dim, NT), a.S);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
     const int threads = (kTCons + 1) * 32;
 #define TRG_S2(MTW, NTV)                                                  \
@@ -408,7 +447,8 @@ void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double*
     a.q = q;
     a.ldq = ldq;
     const int NT = a.K <= 8 ? 1 : 2;
-    const size_t smem = ttm_smem(p.dim);
+    a.S = stages_for(ttm_stage(p.dim));
+    const size_t smem = slab_smem(ttm_stage(p.dim), a.S);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
     const int threads = (kTCons + 1) * 32;
 #define TRG_T2(NTV, TKV)                                                  \

@@ -33,7 +33,7 @@ constexpr int kSkCons = 8;  // consumer warps (sketch): 2 per SM sub-partition k
 #define TRG_SK_RNG 16
 #endif
 #ifndef TRG_SK_ILP
-#define TRG_SK_ILP 1
+#define TRG_SK_ILP 2
 #endif
 constexpr int kRng = TRG_SK_RNG;  // Omega generator warps (sketch): one Box-Muller pair per thread per tile
 constexpr int kIlp = TRG_SK_ILP;  // independent pairs per generator thread per iteration
@@ -110,46 +110,49 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     }
     if (warp >= kSkCons) {
         // ---------------- generator warps: Omega tile in B-fragment order.
-        // kIlp independent Box-Muller pairs per thread per iteration; with 16 warps
-        // one pair per thread covers a 64 x 16 tile in a single round.
+        // With 16 warps one pair per thread covers a 64 x 16 tile in a single round.
         const int rt = tid - kSkCons * 32;
         // pairs per k-column of the tile: CT/2 when every column run starts on an
         // even draw (then nothing is wasted), one more otherwise
         const int npmax = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) ? CT / 2 + 1 : CT / 2;
         const int nitems = a.K * npmax;
-        for (int j = 0; j < nl; ++j) {
-            const int b = j % kOB;
-            mbar_wait(&empty_o[b], ((j / kOB) & 1) ^ 1);
-            const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
-            const int64_t c0 = t * CT;
-            const int64_t ncol = imin64(CT, a.ncols - c0);
-            double* O = omega + b * omega_elems;
-            for (int it0 = rt; it0 < nitems; it0 += kIlp * kRng * 32) {
+        // kIlp tiles per iteration: each thread runs kIlp independent Box-Muller chains (one per
+        // tile), which hides the chains' fp64 latency behind each other (the FP64 datapath is
+        // shared with the consumers' DMMAs, which stretches every dependent step)
+        for (int j = 0; j < nl; j += kIlp) {
+            const int ntl = (int)min((int64_t)kIlp, (int64_t)(nl - j));
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u)
+                if (u < ntl) mbar_wait(&empty_o[(j + u) % kOB], (((j + u) / kOB) & 1) ^ 1);
+            for (int it = rt; it < nitems; it += kRng * 32) {
+                const int k = it / npmax;
+                const int jj = it - k * npmax;
                 double z[kIlp][2];
-                int kk[kIlp];
                 int64_t cc[kIlp];
                 bool live[kIlp];
 #pragma unroll
                 for (int u = 0; u < kIlp; ++u) {
-                    const int it = it0 + u * kRng * 32;
-                    const int k = it / npmax;
-                    const int jj = it - k * npmax;
+                    const int64_t c0 = (blockIdx.x + (int64_t)(j + u) * gridDim.x) * CT;
                     const uint64_t s0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)k;
                     const uint64_t p = (s0 >> 1) + (uint64_t)jj;
-                    live[u] = it < nitems && p <= ((s0 + (uint64_t)CT - 1ull) >> 1);
-                    kk[u] = k;
+                    live[u] = u < ntl && p <= ((s0 + (uint64_t)CT - 1ull) >> 1);
                     cc[u] = (int64_t)(2ull * p - s0);
                     gauss_pair_tab(a.seed, live[u] ? p : 0ull, *tabs, z[u][0], z[u][1]);
                 }
 #pragma unroll
                 for (int u = 0; u < kIlp; ++u) {
                     if (!live[u]) continue;
+                    const int64_t c0 = (blockIdx.x + (int64_t)(j + u) * gridDim.x) * CT;
+                    const int64_t ncol = imin64(CT, a.ncols - c0);
+                    double* O = omega + ((j + u) % kOB) * omega_elems;
                     const int64_t c = cc[u];
-                    if (c >= 0 && c < CT) O[omega_idx((int)c, kk[u], NT)] = c < ncol ? z[u][0] : 0.0;
-                    if (c + 1 >= 0 && c + 1 < CT) O[omega_idx((int)c + 1, kk[u], NT)] = c + 1 < ncol ? z[u][1] : 0.0;
+                    if (c >= 0 && c < CT) O[omega_idx((int)c, k, NT)] = c < ncol ? z[u][0] : 0.0;
+                    if (c + 1 >= 0 && c + 1 < CT) O[omega_idx((int)c + 1, k, NT)] = c + 1 < ncol ? z[u][1] : 0.0;
                 }
             }
-            mbar_arrive(&full_o[b]);
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u)
+                if (u < ntl) mbar_arrive(&full_o[(j + u) % kOB]);
         }
         return;
     }

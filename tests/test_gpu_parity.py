@@ -116,6 +116,33 @@ def test_sketch_householder_fallback_matches(trg):
     assert orc.rse(x, lifted) < 1e-8  # SPEC.md:304 exact capture
 
 
+def test_deferred_projection_parity(trg):
+    # shapes whose modes >= 1 run the TMA slab kernels may take the deferred path (QR of Y_n on
+    # the side stream, Y_n used for the shrink, R_n^-1 folded into later test matrices and P;
+    # opt-in with TRG_DEFERRED=1): either way the result is the reference projection
+    dims, K = [40, 34, 28, 22], [6, 4, 4, 4]
+    x = tr_tensor(dims, [3, 3, 3, 3], 4, snr=30.0)
+    proj, bases, ys = orc.sketch(x, K, 9)
+    got = trg.sketch(x, trg.ProjectionSpec(K, 9))
+    assert relerr(got.projected, proj) < F64_TOL
+    for n in range(4):
+        assert relerr(got.bases[n], bases[n]) < F64_TOL
+        assert relerr(got.sketches[n], ys[n]) < F64_TOL
+
+
+def test_deferred_projection_householder_redo(trg):
+    # rank-2 unfoldings with K = 6: Y_0 is rank deficient, so the deferred substitution is
+    # invalid; the projection must be recomputed eagerly when read and still capture X exactly
+    rng = np.random.default_rng(5)
+    U = [np.linalg.qr(rng.standard_normal((30, 2)))[0] for _ in range(3)]
+    x = np.einsum("abc,ia,jb,kc->ijk", rng.standard_normal((2, 2, 2)), *U)
+    sk = trg.DeviceSketch(trg.default_context(), trg.DeviceTensor.from_numpy(trg.default_context(), x),
+                          trg.ProjectionSpec([6, 6, 6], 2))
+    res = sk.result()
+    assert res.qr_householder[0] == 1
+    assert orc.rse(x, orc.lift_back(res.projected, res.bases)) < 1e-8
+
+
 def test_sketch_determinism(trg):
     x = tr_tensor([50, 40, 30], [3, 3, 3], 8, snr=20.0)
     a = trg.sketch(x, trg.ProjectionSpec([7, 6, 5], 3))

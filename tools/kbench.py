@@ -28,5 +28,26 @@ def bench_qr(iters=50):
         print(f"qr m={m:5d} k={k:3d}: {1e3 * tot / n:8.1f} us/launch")
 
 
-if __name__ == "__main__":
-    {"qr": bench_qr}[sys.argv[1]]()
+if __name__ == "__main__" and sys.argv[1] == "qr":
+    bench_qr()
+
+
+def bench_launch_gap(n=200):
+    """Back-to-back dependent tiny kernels on one stream: device time per launch."""
+    import torch
+
+    x = torch.zeros(1, device="cuda")
+    for _ in range(10):
+        x.add_(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        x.add_(1)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"launch gap: {1e3 * e0.elapsed_time(e1) / n:.2f} us per dependent tiny kernel")
+
+
+if __name__ == "__main__" and sys.argv[1] == "gap":
+    bench_launch_gap()
