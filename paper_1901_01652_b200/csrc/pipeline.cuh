@@ -63,3 +63,18 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 
 }  // namespace trg
+
+namespace trg {
+
+// ---- programmatic dependent launch (PDL) for the per-mode kernel chain
+// Kernels launched with pdl_launch() may be scheduled while their stream predecessor is still
+// running; they must execute griddep_wait() before touching global memory (it returns once
+// the predecessor grid has completed and its writes are visible). Predecessors call
+// griddep_launch_dependents() when their main loop is done, so the dependent grid's launch
+// and CTA rasterisation overlap the predecessor's epilogue instead of following it.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+}  // namespace trg

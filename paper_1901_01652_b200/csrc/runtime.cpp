@@ -193,6 +193,45 @@ struct trg_ctx {
     void dfree(void* p) {
         if (p) cudaFreeAsync(p, stream);
     }
+    // ---- per-projection scratch arena: temporaries of run_sketch (split-K partials, QR work,
+    // intermediate P^(n), test-matrix blocks) come from one context-owned buffer, so no
+    // allocator operation sits between the kernels of the per-mode chain (they are launched
+    // with programmatic dependent launch). Reuse across projections is stream-ordered.
+    char* scr_base = nullptr;
+    size_t scr_cap = 0, scr_off = 0, scr_need = 0;
+    bool scr_active = false;
+    std::vector<void*> scr_overflow;
+    void scr_begin() {
+        if (scr_need > scr_cap) {
+            if (scr_base) cudaFreeAsync(scr_base, stream);
+            scr_cap = scr_need + scr_need / 4;
+            CK(cudaMallocAsync((void**)&scr_base, scr_cap, stream));
+        }
+        scr_off = 0;
+        scr_active = true;
+    }
+    void* tmp(size_t bytes) {
+        if (!scr_active) return alloc(bytes);
+        bytes = (bytes + 255) & ~size_t(255);
+        if (scr_off + bytes > scr_need) scr_need = scr_off + bytes;
+        if (scr_base && scr_off + bytes <= scr_cap) {
+            void* p = scr_base + scr_off;
+            scr_off += bytes;
+            return p;
+        }
+        scr_off += bytes;  // counted for the next projection's arena size
+        void* p = alloc(bytes);
+        scr_overflow.push_back(p);
+        return p;
+    }
+    void tmp_free(void* p) {
+        if (!scr_active) dfree(p);  // arena memory is released wholesale by scr_end()
+    }
+    void scr_end() {
+        for (void* p : scr_overflow) dfree(p);
+        scr_overflow.clear();
+        scr_active = false;
+    }
     void allreduce(void* buf, size_t count, int dtype) {
         if (world == 1 || count == 0) return;
         nccl().check(nccl().allReduce(buf, buf, count, dtype == F64 ? ncclFloat64 : ncclFloat32, ncclSum, comm, stream),
@@ -339,6 +378,7 @@ std::vector<ModeOffsets> sketch_offsets(const std::vector<int64_t>& dims, const 
 struct PreOmega {
     double* buf = nullptr;
     cudaEvent_t ready = nullptr;
+    bool joined = false;  // main stream already waits on `ready`
 };
 
 void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
@@ -355,10 +395,10 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     p.rows_glob = off.rows_glob;
     p.col_off = off.col_off;
     const bool sharded_rows = (n == N - 1) && ctx->world > 1;
-    double* ylocal = sharded_rows ? (double*)ctx->alloc(sizeof(double) * p.dim * Kn) : dYfull;
+    double* ylocal = sharded_rows ? (double*)ctx->tmp(sizeof(double) * p.dim * Kn) : dYfull;
     double* partial = nullptr;
     if (trg::stream_sketch_ok(p.dtype, p.left, p.dim, (int)Kn)) {
-        partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
         int grid = 0;
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_stream_sketch(p, cur, partial, ylocal, ctx->num_sms, &grid, ctx->stream);
@@ -366,7 +406,7 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     } else if (trg::stream_sketch_f32_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
         int gc = 0;
         trg::stream_sketch_f32_grid(p.dim, (int)Kn, p.right, ctx->num_sms, &gc);
-        partial = (double*)ctx->alloc(sizeof(double) * gc * p.dim * Kn);
+        partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_stream_sketch_f32(p, cur, partial, ylocal, ctx->num_sms, ctx->stream);
         }, 2);
@@ -375,37 +415,37 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
         double* om = nullptr;
         if (pre && pre->buf) {
             om = pre->buf;
-            CK(cudaStreamWaitEvent(ctx->stream, pre->ready, 0));
+            if (pre->ready && !pre->joined) CK(cudaStreamWaitEvent(ctx->stream, pre->ready, 0));
         } else {
-            om = (double*)ctx->alloc(sizeof(double) * trg::slab2_units(p.left, p.right) * 4 * NT * 32);
+            om = (double*)ctx->tmp(sizeof(double) * trg::slab2_units(p.left, p.right) * 4 * NT * 32);
             ctx->launch("omega_m" + std::to_string(n), [&] {
                 trg::launch_omega_units(p.left, p.right, (int)Kn, p.seed, p.D, p.col_off, p.rows_glob, om,
                                         ctx->stream);
             }, 2);
         }
-        partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_slab2_sketch(p, cur, om, partial, ylocal, ctx->num_sms, ctx->stream);
         }, 2);
-        ctx->dfree(om);
+        if (!(pre && pre->buf)) ctx->tmp_free(om);  // pre-generated blocks live in the arena
         if (pre) pre->buf = nullptr;
     } else if (trg::slab_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.left * p.right)) {
-        partial = (double*)ctx->alloc(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
         ctx->launch("sketch_m" + std::to_string(n), [&] {
             trg::launch_slab_sketch(p, cur, partial, ylocal, ctx->num_sms, ctx->stream);
         }, 2);
     } else {
         trg::plan_sketch(p, ctx->num_sms);
-        partial = (double*)ctx->alloc(p.partial_elems * sizeof(double));
+        partial = (double*)ctx->tmp(p.partial_elems * sizeof(double));
         ctx->launch("sketch_m" + std::to_string(n), [&] { trg::launch_sketch(p, cur, partial, ylocal, ctx->stream); },
                     2);
     }
-    ctx->dfree(partial);
+    ctx->tmp_free(partial);
     if (sharded_rows) {
         ctx->launch("scatter", [&] {
             trg::launch_scatter_rows(ylocal, p.dim, (int)Kn, x->lo, x->dims[n], dYfull, ctx->stream);
         });
-        ctx->dfree(ylocal);
+        ctx->tmp_free(ylocal);
     }
     ctx->allreduce(dYfull, (size_t)(x->dims[n] * Kn), F64);
 }
@@ -413,7 +453,7 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
 // out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
 // out = cur x_n Q^T; *odt is the output dtype (fp32 mode-0 input is promoted to fp64 by its shrink)
 void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
-                  int n, int64_t Kn, const double* dQ, int* odt) {
+                  int n, int64_t Kn, const double* dQ, int* odt, bool escape = true) {
     const int N = (int)cur_shape.size();
     trg::TTMPlan p{};
     p.dtype = cdt;
@@ -428,7 +468,7 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
     const bool promote = trg::stream_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right);
     *odt = promote ? F64 : cdt;
     const size_t es = trg::dtype_size(*odt);
-    void* out = ctx->alloc(es * (size_t)(p.left * Kn * p.right));
+    void* out = escape ? ctx->alloc(es * (size_t)(p.left * Kn * p.right)) : ctx->tmp(es * (size_t)(p.left * Kn * p.right));
     if (promote) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm_f32(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
@@ -465,7 +505,7 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const s
         const int64_t left = prod(shape, 0, m), dim = shape[m], right = prod(shape, m + 1);
         if (left > 1 && trg::slab2_ok(later_dt, left, dim, K[m], right)) {
             const int NT = K[m] <= 8 ? 1 : 2;
-            pre[m].buf = (double*)ctx->alloc(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
+            pre[m].buf = (double*)ctx->tmp(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
             CK(cudaEventRecord(go, ctx->stream));
             CK(cudaStreamWaitEvent(ctx->side, go, 0));
             trg::launch_omega_units(left, right, (int)K[m], seed, offs[m].D, offs[m].col_off, offs[m].rows_glob,
@@ -660,19 +700,32 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     }
     sk->deferred = false;
     sk->checked = true;
+    ctx->scr_begin();
 
     int cdt = x->dtype;  // dtype of the working tensor (fp32 input is promoted by its mode-0 shrink)
     std::vector<int64_t> shape = x->local_shape();
     const void* cur = x->d;
-    void* owned = nullptr;  // buffer owned by the pipeline (not x)
+    void* owned = nullptr;      // buffer owned by the pipeline (not x)
+    bool owned_arena = false;   // ... and whether it lives in the scratch arena
     const std::vector<ModeOffsets> offs = sketch_offsets(x->dims, Kin, x->lo, variant);
+    int last_proj = -1, first_proj = -1;
+    for (int n = 0; n < N; ++n)
+        if (sk->K[n] != x->dims[n]) {
+            last_proj = n;
+            if (first_proj < 0) first_proj = n;
+            // escaping outputs first, so no allocator call sits between the chain's kernels
+            sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * sk->K[n]);
+            sk->dQ[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * sk->K[n]);
+        }
+    auto release_owned = [&]() {
+        if (owned && !owned_arena) ctx->dfree(owned);
+    };
 
     auto qr = [&](int n) {
         const int64_t In = x->dims[n], Kn = sk->K[n];
-        double* work = (double*)ctx->alloc(sizeof(double) * In * Kn);
-        sk->dQ[n] = (double*)ctx->alloc(sizeof(double) * In * Kn);
+        double* work = (double*)ctx->tmp(sizeof(double) * In * Kn);
         ctx->launch("qr", [&] { trg::launch_qr(sk->dY[n], In, (int)Kn, sk->dQ[n], work, sk->dflags + n, ctx->stream); });
-        ctx->dfree(work);
+        ctx->tmp_free(work);
     };
 
     std::vector<PreOmega> pre(N);
@@ -682,10 +735,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
-            if (!y_ready[n]) {
-                sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
-                sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n]);
-            }
+            if (!y_ready[n]) sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n]);
             if (!pre_started) {
                 // Omega_m of every later slab-kernel mode depends only on shapes and the seed:
                 // generate them on the side stream while this mode's QR (one SM) and
@@ -695,7 +745,17 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre);
             }
             qr(n);
+            if (n == first_proj) {
+                // join the side stream once, here, rather than before every later sketch: each
+                // cross-stream wait would cut a programmatic-dependent-launch edge of the chain
+                for (auto& po : pre)
+                    if (po.ready) {
+                        CK(cudaStreamWaitEvent(ctx->stream, po.ready, 0));
+                        po.joined = true;
+                    }
+            }
             void* out = nullptr;
+            const bool escape = n == last_proj;  // the last shrink writes P itself
             // K3: fuse this shrink with the next mode's sketch while P^(1) tiles are on chip
             // off by default: the separate shrink + TMA slab sketch measure faster (profiles/)
             static const bool fuse = getenv("TRG_FUSE") != nullptr;
@@ -712,25 +772,28 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 fp.D1 = offs[1].D;
                 fp.rows_glob1 = offs[1].rows_glob;
                 fp.col_off1 = offs[1].col_off;
-                out = ctx->alloc(trg::dtype_size(cdt) * (size_t)(Kn * prod(shape, 1)));
-                sk->dY[1] = (double*)ctx->alloc(sizeof(double) * x->dims[1] * sk->K[1]);
+                out = ctx->tmp(trg::dtype_size(cdt) * (size_t)(Kn * prod(shape, 1)));
                 const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(fp.nfib, ctx->num_sms));
-                double* partial = (double*)ctx->alloc(sizeof(double) * grid * fp.I1 * fp.K1);
+                double* partial = (double*)ctx->tmp(sizeof(double) * grid * fp.I1 * fp.K1);
                 ctx->launch("ttm_m0+sketch_m1", [&] {
                     trg::launch_fused_ttm_sketch(fp, cur, out, sk->dQ[0], partial, sk->dY[1], ctx->num_sms,
                                                  ctx->stream);
                 }, 2);
-                ctx->dfree(partial);
+                ctx->tmp_free(partial);
                 ctx->allreduce(sk->dY[1], (size_t)(x->dims[1] * sk->K[1]), F64);
                 y_ready[1] = true;
+                release_owned();
+                owned = out;
+                owned_arena = true;
             } else {
                 int odt = cdt;
-                out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt);
+                out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt, escape);
                 cdt = odt;
+                release_owned();
+                owned = out;
+                owned_arena = !escape;
             }
             if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), cdt);
-            if (owned) ctx->dfree(owned);
-            owned = out;
             cur = out;
             shape[n] = Kn;
         }
@@ -741,7 +804,6 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
-            sk->dY[n] = (double*)ctx->alloc(sizeof(double) * x->dims[n] * Kn);
             sketch_mode(ctx, x, x->dtype, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n]);
             qr(n);
         }
@@ -749,11 +811,13 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
             int odt = cdt;
-            void* out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt);
+            const bool escape = n == last_proj;
+            void* out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt, escape);
             cdt = odt;
             if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), cdt);
-            if (owned) ctx->dfree(owned);
+            release_owned();
             owned = out;
+            owned_arena = !escape;
             cur = out;
             shape[n] = Kn;
         }
@@ -769,10 +833,19 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         CK(cudaMemcpyAsync((char*)g + es * inner * x->lo, cur, es * inner * (x->hi - x->lo), cudaMemcpyDeviceToDevice,
                            ctx->stream));
         ctx->allreduce(g, (size_t)full, cdt);
-        if (owned) ctx->dfree(owned);
+        release_owned();
         owned = g;
+        owned_arena = false;
         cur = g;
         shape[N - 1] = x->dims[N - 1];
+    }
+    if (owned && owned_arena) {  // P must outlive the arena (fused path / odd cases): copy it out
+        const size_t bytes = trg::dtype_size(cdt) * (size_t)prod(shape);
+        void* p2 = ctx->alloc(bytes);
+        CK(cudaMemcpyAsync(p2, owned, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+        owned = p2;
+        owned_arena = false;
+        cur = p2;
     }
     sk->P_elems = prod(shape);
     sk->dtype = cdt;  // P's dtype (fp64 once an fp32 input has been promoted)
@@ -783,10 +856,9 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         sk->dP = const_cast<void*>(cur);  // no mode projected: P is x itself (sketch.hpp:71)
         sk->P_is_view = true;
     }
-    for (auto& po : pre) {
-        if (po.buf) ctx->dfree(po.buf);  // mode not reached (cannot happen unless it failed validation)
+    for (auto& po : pre)
         if (po.ready) cudaEventDestroy(po.ready);  // destruction is deferred until the event completes
-    }
+    ctx->scr_end();
     CK(cudaEventRecord(sk->ev1, ctx->stream));
 }
 
@@ -1166,6 +1238,7 @@ int trg_ctx_destroy(trg_ctx* ctx) {
         for (auto e : ctx->event_pool) cudaEventDestroy(e);
         if (ctx->comm) nccl().commDestroy(ctx->comm);
         cudaStreamSynchronize(ctx->side);
+        if (ctx->scr_base) cudaFree(ctx->scr_base);
         cudaStreamDestroy(ctx->side);
         cudaStreamDestroy(ctx->stream);
         delete ctx;

@@ -20,6 +20,8 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "pipeline.cuh"
+#include "launch.h"
 
 namespace trg {
 
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(256) k_sketch(SketchArgs a) {
 __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ partial, int nblocks, int64_t n,
                                                          double* __restrict__ out) {
     __shared__ double red[8][32];
+    griddep_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * 32 + lane;
     double s = 0.0;
@@ -299,7 +302,7 @@ const GaussTables* gauss_tables(cudaStream_t s) {
 
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s) {
     const int blocks = (int)std::max<int64_t>(1, (n + 31) / 32);
-    k_reduce_partials<<<blocks, 256, 0, s>>>(partial, nblocks, n, out);
+    pdl_launch(k_reduce_partials, dim3(blocks), dim3(256), 0, s, partial, nblocks, n, out);
 }
 
 void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, double* out, cudaStream_t s) {

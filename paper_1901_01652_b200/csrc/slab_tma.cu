@@ -33,6 +33,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.h"
 #include "pipeline.cuh"
 
 namespace trg {
@@ -106,6 +107,7 @@ template <int MTW, int NT>
 __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     k_slab2_sketch_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    griddep_wait();
     const int dim = (int)a.dim;
     const int rows_pad = (dim + 7) & ~7;
     const int xbytes = rows_pad * 128;  // multiple of 1024: keeps every stage swizzle-aligned
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         mbar_arrive(&empty[s]);
     }
     // fixed-order sum of the consumer warps' partials through stage 0 (all consumed)
+    griddep_launch_dependents();
     asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
     double* red = reinterpret_cast<double*>(base);
     const int ld = 8 * a.mtiles;
@@ -217,6 +220,7 @@ template <int NT, int TKM>
 __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     k_slab2_ttm_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    griddep_wait();
     const int dim = (int)a.dim;
     const int rows_pad = (dim + 7) & ~7;
     const int sbytes = rows_pad * 128;
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     const int pair = warp & 3, mt = warp >> 2;  // pair takes units j = pair (mod 4); mt = 8-row tile of l
     for (int64_t j = pair; j < nl; j += 4) {
         const int s = (int)(j % kStg);
+        if (j + 4 >= nl) griddep_launch_dependents();  // this pair's last unit
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
         const double* X = reinterpret_cast<const double*>(base + s * sbytes);
         double acc[2][NT][2];  // [k-step parity][column tile][pair]
@@ -420,7 +425,7 @@ void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega
 #define TRG_S2(MTW, NTV)                                                  \
     do {                                                                  \
         set_smem(k_slab2_sketch_f64<MTW, NTV>, smem);                     \
-        k_slab2_sketch_f64<MTW, NTV><<<grid, threads, smem, s>>>(map, a); \
+        pdl_launch(k_slab2_sketch_f64<MTW, NTV>, dim3(grid), dim3(threads), smem, s, map, a); \
     } while (0)
     if (a.mtiles <= 8) {
         if (NT == 1) TRG_S2(4, 1); else TRG_S2(4, 2);
@@ -454,7 +459,7 @@ void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double*
 #define TRG_T2(NTV, TKV)                                                  \
     do {                                                                  \
         set_smem(k_slab2_ttm_f64<NTV, TKV>, smem);                        \
-        k_slab2_ttm_f64<NTV, TKV><<<grid, threads, smem, s>>>(map, a);    \
+        pdl_launch(k_slab2_ttm_f64<NTV, TKV>, dim3(grid), dim3(threads), smem, s, map, a); \
     } while (0)
     if (a.Tk <= 16) {
         if (NT == 1) TRG_T2(1, 16); else TRG_T2(2, 16);

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.h"
 #include "pipeline.cuh"
 
 namespace trg {
@@ -59,6 +60,7 @@ __device__ __forceinline__ int omega_idx(int c, int k, int NT) {
 template <int MTW, int NT>
 __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(SkArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    griddep_wait();
     const int CT = a.CT;
     const int64_t dim = a.dim;
     const int stage_elems = (int)(CT * dim) + kPad;
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     }
     // fixed-order reduction over the 4 k-step groups through (consumed) stage 0;
     // the two halves of a group write disjoint rows
+    griddep_launch_dependents();
     asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
     double* red = stages;
     const int ld = 8 * a.mtiles;
@@ -552,6 +555,7 @@ __global__ void __launch_bounds__((kFCons + kFGen + 1) * 32, 1) k_ttm_sketch_l1_
 template <int MTO, int TKM>
 __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    griddep_wait();
     const int64_t dim = a.dim;
     const int MT = a.MT;
     const int stage_elems = (int)(MT * dim) + kPad;
@@ -601,6 +605,7 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
     }
     for (int j = 0; j < nl; ++j) {
         const int s = j % kStages;
+        if (j == nl - 1) griddep_launch_dependents();  // last tile: let the next kernel's launch overlap
         mbar_wait(&full_x[s], (j / kStages) & 1);
         // B fragment: X^T(d = 4t + r, row = 8 nt + q) = X[row][d]
         const double* x0 = stages + s * stage_elems + (16 * warp + q) * dim + r;
@@ -689,7 +694,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
 #define TRG_SK(MTW, NTV)                                                 \
     do {                                                                 \
         set_smem(k_sketch_l1_f64<MTW, NTV>, smem);                       \
-        k_sketch_l1_f64<MTW, NTV><<<grid, threads, smem, s>>>(a);        \
+        pdl_launch(k_sketch_l1_f64<MTW, NTV>, dim3(grid), dim3(threads), smem, s, a); \
     } while (0)
 #define TRG_SK_NT(MTW)                   \
     switch (NT) {                        \
@@ -741,7 +746,7 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
 #define TRG_QR(MTO, TKM)                                                  \
     do {                                                                  \
         set_smem(k_ttm_qreg_f64<MTO, TKM>, smem);                         \
-        k_ttm_qreg_f64<MTO, TKM><<<grid, threads, smem, s>>>(a);          \
+        pdl_launch(k_ttm_qreg_f64<MTO, TKM>, dim3(grid), dim3(threads), smem, s, a); \
     } while (0)
         if (a.K <= 8) {
             if (a.Tk <= 16) TRG_QR(1, 16); else if (a.Tk <= 25) TRG_QR(1, 25); else TRG_QR(1, 32);
