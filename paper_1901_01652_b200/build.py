@@ -29,7 +29,7 @@ def _flags():
         "-Xptxas", "-v" if os.environ.get("TRG_PTXAS_VERBOSE") else "-O3",
         "-ccbin", "g++",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-    ]
+    ] + os.environ.get("TRG_EXTRA_NVCC", "").split()
 
 
 def _headers():

@@ -49,6 +49,8 @@ void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cu
 
 // ---- TMA-pipelined fp64 tensor-core kernels for the mode-0 passes (stream_f64.cu)
 bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K);
+// The per-CTA partial sums of Y go to `partial`; with y == nullptr the split-K reduction is
+// left to the caller (launch_qr_fused), and the launchers return the number of partials.
 void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
                           int* grid_out, cudaStream_t s);
 bool stream_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t odim);
@@ -57,8 +59,8 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
 // ---- fp32 mode-0 sketch (FFMA, TMA 2-D boxes), stream_f32.cu; partial = grid_cols x dim x K
 bool stream_sketch_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
 int stream_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms, int* grid_cols);
-void launch_stream_sketch_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
-                              cudaStream_t s);
+int launch_stream_sketch_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                             cudaStream_t s);
 bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols);
 // writes P^(1) in fp64 (the fp32 input's later modes then run the fp64 kernels)
 void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
@@ -90,16 +92,24 @@ void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint6
                         int64_t rows_glob, double* out, cudaStream_t s);
 // standard-layout test matrix (rows left*right, K columns) -> unit blocks
 void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s);
-void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
-                         int num_sms, cudaStream_t s);
+int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
+                        int num_sms, cudaStream_t s);
 void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                       cudaStream_t s);
 // fixed-order sum of nblocks partial (n doubles each)
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s);
+// the same sum (fixed order, a different one) spread over ~n / 16 CTAs with 16-byte loads
+void launch_reduce_wide(const double* partial, int nparts, int64_t n, double* out, cudaStream_t s);
 
 // ---- thin QR with diag(R) >= 0 (K4): CholQR2 + Householder fallback, fp64.
 // Y is m x k column-major; Q (m x k) out. work >= m*k doubles + 2*k.
 void launch_qr(const double* y, int64_t m, int k, double* q, double* work, int* flag, cudaStream_t s);
+// Split-K reduction of nparts partial sums of Y (m x k each) fused with its QR in one cluster
+// launch; writes Y and Q. Returns false (nothing launched) when the shape is outside the
+// fused kernel (k > 32 or the staging does not fit), then the caller reduces and calls launch_qr.
+bool qr_fused_ok(int64_t m, int k);
+int launch_qr_fused(const double* part, int nparts, int64_t m, int k, double* y, double* q, double* work, int* flag,
+                    cudaStream_t s);  // returns the number of kernels launched
 // Rinv = (upper(Q^T Y))^-1, k x k col-major, so that Q = Y Rinv; *bad set if R is near-singular
 void launch_rinv(const double* q, const double* y, int64_t m, int k, double* rinv, int* bad, cudaStream_t s);
 

@@ -381,8 +381,15 @@ struct PreOmega {
     bool joined = false;  // main stream already waits on `ready`
 };
 
+// Per-CTA partial sums of Y_n left for the QR launch to reduce (launch_qr_fused)
+struct YParts {
+    double* partial = nullptr;
+    int nparts = 0;
+};
+
 void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
-                 int n, int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull, PreOmega* pre = nullptr) {
+                 int n, int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull, PreOmega* pre = nullptr,
+                 YParts* yp = nullptr) {
     const int N = (int)cur_shape.size();
     trg::SketchPlan p{};
     p.dtype = cdt;
@@ -397,19 +404,25 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     const bool sharded_rows = (n == N - 1) && ctx->world > 1;
     double* ylocal = sharded_rows ? (double*)ctx->tmp(sizeof(double) * p.dim * Kn) : dYfull;
     double* partial = nullptr;
+    // single rank: the split-K reduction of Y_n moves into the QR launch (one cluster kernel)
+    static const bool no_fuse_qr = getenv("TRG_QR_LEGACY") != nullptr;
+    const bool defer = yp && ctx->world == 1 && !no_fuse_qr && trg::qr_fused_ok(p.dim, (int)Kn);
+    double* yout = defer ? nullptr : ylocal;
     if (trg::stream_sketch_ok(p.dtype, p.left, p.dim, (int)Kn)) {
         partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
         int grid = 0;
         ctx->launch("sketch_m" + std::to_string(n), [&] {
-            trg::launch_stream_sketch(p, cur, partial, ylocal, ctx->num_sms, &grid, ctx->stream);
-        }, 2);
+            trg::launch_stream_sketch(p, cur, partial, yout, ctx->num_sms, &grid, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, grid};
     } else if (trg::stream_sketch_f32_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
         int gc = 0;
         trg::stream_sketch_f32_grid(p.dim, (int)Kn, p.right, ctx->num_sms, &gc);
         partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
         ctx->launch("sketch_m" + std::to_string(n), [&] {
-            trg::launch_stream_sketch_f32(p, cur, partial, ylocal, ctx->num_sms, ctx->stream);
-        }, 2);
+            gc = trg::launch_stream_sketch_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, gc};
     } else if (p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
         const int NT = Kn <= 8 ? 1 : 2;
         double* om = nullptr;
@@ -424,9 +437,11 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
             }, 2);
         }
         partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
+        int grid = 0;
         ctx->launch("sketch_m" + std::to_string(n), [&] {
-            trg::launch_slab2_sketch(p, cur, om, partial, ylocal, ctx->num_sms, ctx->stream);
-        }, 2);
+            grid = trg::launch_slab2_sketch(p, cur, om, partial, yout, ctx->num_sms, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, grid};
         if (!(pre && pre->buf)) ctx->tmp_free(om);  // pre-generated blocks live in the arena
         if (pre) pre->buf = nullptr;
     } else if (trg::slab_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.left * p.right)) {
@@ -440,7 +455,7 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
         ctx->launch("sketch_m" + std::to_string(n), [&] { trg::launch_sketch(p, cur, partial, ylocal, ctx->stream); },
                     2);
     }
-    ctx->tmp_free(partial);
+    if (!defer) ctx->tmp_free(partial);  // else freed after the QR launch reduced it
     if (sharded_rows) {
         ctx->launch("scatter", [&] {
             trg::launch_scatter_rows(ylocal, p.dim, (int)Kn, x->lo, x->dims[n], dYfull, ctx->stream);
@@ -721,10 +736,20 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         if (owned && !owned_arena) ctx->dfree(owned);
     };
 
+    std::vector<YParts> yparts(N);
     auto qr = [&](int n) {
         const int64_t In = x->dims[n], Kn = sk->K[n];
         double* work = (double*)ctx->tmp(sizeof(double) * In * Kn);
-        ctx->launch("qr", [&] { trg::launch_qr(sk->dY[n], In, (int)Kn, sk->dQ[n], work, sk->dflags + n, ctx->stream); });
+        if (yparts[n].partial) {
+            ctx->launch("qr", [&] {
+                trg::launch_qr_fused(yparts[n].partial, yparts[n].nparts, In, (int)Kn, sk->dY[n], sk->dQ[n], work,
+                                     sk->dflags + n, ctx->stream);
+            }, yparts[n].nparts > 1 ? 2 : 1);
+            ctx->tmp_free(yparts[n].partial);
+            yparts[n] = YParts{};
+        } else {
+            ctx->launch("qr", [&] { trg::launch_qr(sk->dY[n], In, (int)Kn, sk->dQ[n], work, sk->dflags + n, ctx->stream); });
+        }
         ctx->tmp_free(work);
     };
 
@@ -735,7 +760,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
-            if (!y_ready[n]) sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n]);
+            if (!y_ready[n]) sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n]);
             if (!pre_started) {
                 // Omega_m of every later slab-kernel mode depends only on shapes and the seed:
                 // generate them on the side stream while this mode's QR (one SM) and
@@ -804,7 +829,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
-            sketch_mode(ctx, x, x->dtype, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n]);
+            sketch_mode(ctx, x, x->dtype, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n], nullptr, &yparts[n]);
             qr(n);
         }
         for (int n = 0; n < N; ++n) {

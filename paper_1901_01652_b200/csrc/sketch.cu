@@ -176,6 +176,49 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restric
     }
 }
 
+// Split-K reduction spread over many SMs: CTA c owns kRwUnits units (pairs of entries when the
+// partial blocks allow 16-byte loads); its threads split the partials into kRwGroups strided
+// groups, issue all of their loads, and the groups are summed in a fixed order.
+constexpr int kRwThreads = 256, kRwUnits = 8, kRwGroups = kRwThreads / kRwUnits;
+__global__ void __launch_bounds__(kRwThreads) k_reduce_wide(const double* __restrict__ partial, int nparts, int64_t n,
+                                                            int vec, double* __restrict__ out) {
+    __shared__ double2 red[kRwGroups][kRwUnits];
+    griddep_wait();
+    const int w = threadIdx.x % kRwUnits, g = threadIdx.x / kRwUnits;
+    const int64_t u = (int64_t)blockIdx.x * kRwUnits + w;
+    const int64_t nu = vec ? n / 2 : n;
+    double2 sacc = make_double2(0.0, 0.0);
+    if (u < nu) {
+        if (vec) {
+            const double2* pp = reinterpret_cast<const double2*>(partial) + u;
+#pragma unroll 8
+            for (int b = g; b < nparts; b += kRwGroups) {
+                const double2 v = pp[(int64_t)b * (n / 2)];
+                sacc.x += v.x;
+                sacc.y += v.y;
+            }
+        } else {
+#pragma unroll 8
+            for (int b = g; b < nparts; b += kRwGroups) sacc.x += partial[(int64_t)b * n + u];
+        }
+    }
+    red[g][w] = sacc;
+    __syncthreads();
+    if (g == 0 && u < nu) {
+        double2 t = red[0][w];
+        for (int g2 = 1; g2 < kRwGroups; ++g2) {
+            t.x += red[g2][w].x;
+            t.y += red[g2][w].y;
+        }
+        if (vec) {
+            out[2 * u] = t.x;
+            out[2 * u + 1] = t.y;
+        } else {
+            out[u] = t.x;
+        }
+    }
+}
+
 __global__ void k_gauss_tables(GaussTables* t) {
     const int i = threadIdx.x;
     if (i < 128) {
@@ -303,6 +346,13 @@ const GaussTables* gauss_tables(cudaStream_t s) {
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s) {
     const int blocks = (int)std::max<int64_t>(1, (n + 31) / 32);
     pdl_launch(k_reduce_partials, dim3(blocks), dim3(256), 0, s, partial, nblocks, n, out);
+}
+
+void launch_reduce_wide(const double* partial, int nparts, int64_t n, double* out, cudaStream_t s) {
+    const int vec = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(partial) % 16 == 0);
+    const int64_t nu = vec ? n / 2 : n;
+    const int blocks = (int)std::max<int64_t>(1, (nu + kRwUnits - 1) / kRwUnits);
+    pdl_launch(k_reduce_wide, dim3(blocks), dim3(kRwThreads), 0, s, partial, nparts, n, vec, out);
 }
 
 void launch_omega(uint64_t seed, uint64_t off, int64_t rows, int64_t cols, double* out, cudaStream_t s) {

@@ -273,7 +273,6 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     const int pair = warp & 3, mt = warp >> 2;  // pair takes units j = pair (mod 4); mt = 8-row tile of l
     for (int64_t j = pair; j < nl; j += 4) {
         const int s = (int)(j % kStg);
-        if (j + 4 >= nl) griddep_launch_dependents();  // this pair's last unit
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
         const double* X = reinterpret_cast<const double*>(base + s * sbytes);
         double acc[2][NT][2];  // [k-step parity][column tile][pair]
@@ -403,7 +402,7 @@ void launch_pack_units(const double* om, int64_t left, int64_t right, int K, dou
     k_pack_units<<<blocks, 256, 0, s>>>(om, left * right, left, LC, nunits, K, NT, out);
 }
 
-void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
+int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
                          int num_sms, cudaStream_t s) {
     CUtensorMap map;
     make_map(&map, x, p.left, p.dim * p.right, p.dim);
@@ -433,7 +432,8 @@ void launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega
         if (NT == 1) TRG_S2(8, 1); else TRG_S2(8, 2);
     }
 #undef TRG_S2
-    launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
+    if (y) launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
+    return grid;
 }
 
 void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,

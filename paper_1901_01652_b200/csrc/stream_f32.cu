@@ -414,7 +414,7 @@ int stream_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms, int* 
     return *gc * p.DS;
 }
 
-void launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* partial, double* y, int num_sms,
+int launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* partial, double* y, int num_sms,
                               cudaStream_t s) {
     F32Plan p;
     plan_f32(sp.dim, sp.K, p);
@@ -465,7 +465,8 @@ void launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* parti
         default: TRG_F32(24); break;
     }
 #undef TRG_F32
-    launch_reduce_partials(partial, gc, sp.dim * sp.K, y, s);
+    if (y) launch_reduce_partials(partial, gc, sp.dim * sp.K, y, s);
+    return gc;
 }
 
 bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols) {

@@ -31,21 +31,26 @@ constexpr int kStages = 3;
 constexpr int kCons = 4;    // consumer warps (shrink)
 constexpr int kSkCons = 8;  // consumer warps (sketch): 2 per SM sub-partition keep the DMMA pipe fed
 #ifndef TRG_SK_RNG
-#define TRG_SK_RNG 16
+#define TRG_SK_RNG 8
 #endif
 #ifndef TRG_SK_ILP
 #define TRG_SK_ILP 2
 #endif
 constexpr int kRng = TRG_SK_RNG;  // Omega generator warps (sketch): one Box-Muller pair per thread per tile
 constexpr int kIlp = TRG_SK_ILP;  // independent pairs per generator thread per iteration
-constexpr int kOB = 4;      // Omega tile buffers: the generators may run kOB - 1 tiles ahead
+// generator slots per thread per tile on the fast path: a 64 x 16 tile has 512 pairs
+constexpr int kIpt = (512 + kRng * 32 - 1) / (kRng * 32);
+constexpr int kMaxOB = 8;   // Omega tile buffers (sketch), see sk_plan
+constexpr int kMaxStg = 8;  // X stages (sketch)
 constexpr int kPad = 8;   // zeroed doubles after each stage (A rows may overrun by < 8)
-constexpr size_t kBarBytes = 256;  // room for the mbarriers after the buffers
+constexpr size_t kBarBytes = 512;  // room for the mbarriers after the buffers
 
 struct SkArgs {
     const double* x;
     int64_t dim, ncols, ntiles, rows_glob, col_off;
     int K, CT, mtiles;
+    int nstg, nob;  // X stages and Omega buffers in shared memory (sk_plan)
+    int pad;        // zeroed doubles after each stage: every warp reads MTW row tiles unpredicated
     uint64_t seed, D;
     double* partial;
     const GaussTables* gt;
@@ -63,30 +68,39 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     griddep_wait();
     const int CT = a.CT;
     const int64_t dim = a.dim;
-    const int stage_elems = (int)(CT * dim) + kPad;
+    const int nstg = a.nstg, nob = a.nob;
+    const int stage_elems = (int)(CT * dim) + a.pad;
     double* stages = reinterpret_cast<double*>(smem_raw);
     const int omega_elems = CT * NT * 8;
-    double* omega = stages + kStages * stage_elems;
-    GaussTables* tabs = reinterpret_cast<GaussTables*>(omega + kOB * omega_elems);
+    double* omega = stages + nstg * stage_elems;
+    GaussTables* tabs = reinterpret_cast<GaussTables*>(omega + nob * omega_elems);
     uint64_t* bars = reinterpret_cast<uint64_t*>(tabs + 1);
     uint64_t* full_x = bars;
-    uint64_t* empty_x = bars + kStages;
-    uint64_t* full_o = bars + 2 * kStages;
-    uint64_t* empty_o = bars + 2 * kStages + kOB;
+    uint64_t* empty_x = bars + nstg;
+    uint64_t* full_o = bars + 2 * nstg;
+    uint64_t* empty_o = bars + 2 * nstg + nob;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nl = (int)((a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    // Generator mode. Pairs per k-column of a tile: CT/2 when every column run starts on an
+    // even draw (then nothing is wasted), one more otherwise. The fast path (even starts, one
+    // round of the generator threads covers a tile) gives each thread one fixed (column, pair)
+    // slot; a tile is then written by nitems threads.
+    const bool odd = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) != 0;
+    const int npmax = odd ? CT / 2 + 1 : CT / 2;
+    const int nitems = a.K * npmax;
+    const bool fast = !odd && nitems <= kIpt * kRng * 32;
 
-    for (int i = tid; i < kStages * stage_elems; i += blockDim.x) stages[i] = 0.0;
-    for (int i = tid; i < kOB * omega_elems; i += blockDim.x) omega[i] = 0.0;
+    for (int i = tid; i < nstg * stage_elems; i += blockDim.x) stages[i] = 0.0;
+    for (int i = tid; i < nob * omega_elems; i += blockDim.x) omega[i] = 0.0;
     gauss_tables_to_smem(*tabs, a.gt);
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < nstg; ++s) {
             mbar_init(&full_x[s], 1);
             mbar_init(&empty_x[s], kSkCons * 32);
         }
-        for (int b = 0; b < kOB; ++b) {
-            mbar_init(&full_o[b], kRng * 32);
+        for (int b = 0; b < nob; ++b) {
+            mbar_init(&full_o[b], fast ? min(nitems, kRng * 32) : kRng * 32);
             mbar_init(&empty_o[b], kSkCons * 32);
         }
         fence_mbar_init();
@@ -97,15 +111,15 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
         // ---------------- producer: TMA bulk copies of CT whole columns
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            for (int j = 0; j < nl; ++j) {
-                const int s = j % kStages;
-                mbar_wait(&empty_x[s], ((j / kStages) & 1) ^ 1);
+            for (int j = 0, s = 0, ph = 0; j < nl; ++j) {
+                mbar_wait(&empty_x[s], ph ^ 1);
                 const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
                 const int64_t c0 = t * CT;
                 const int64_t ncol = imin64(CT, a.ncols - c0);
                 const uint32_t bytes = (uint32_t)(ncol * dim * 8);
                 mbar_arrive_expect_tx(&full_x[s], bytes);
                 bulk_g2s(stages + s * stage_elems, a.x + c0 * dim, bytes, &full_x[s], pol);
+                if (++s == nstg) s = 0, ph ^= 1;
             }
         }
         return;
@@ -114,10 +128,73 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
         // ---------------- generator warps: Omega tile in B-fragment order.
         // With 16 warps one pair per thread covers a 64 x 16 tile in a single round.
         const int rt = tid - kSkCons * 32;
-        // pairs per k-column of the tile: CT/2 when every column run starts on an
-        // even draw (then nothing is wasted), one more otherwise
-        const int npmax = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) ? CT / 2 + 1 : CT / 2;
-        const int nitems = a.K * npmax;
+        if (fast) {
+            // Thread slot (sub, k, jj) writes rows 2jj, 2jj + 1 of column k of tiles sub, sub + R,
+            // ... of every group of G = R kIlp tiles; with more slots than threads a thread owns
+            // kIpt slots of every tile instead (R = 1). From one tile of this CTA to the next the
+            // pair index advances by gridDim.x * CT / 2, i.e. the SplitMix64 state by
+            // gridDim.x * CT * gamma, so no per-tile index arithmetic is left in the loop.
+            constexpr int nth = kRng * 32;
+            const int R = nitems <= nth ? nth / nitems : 1, G = R * kIlp;
+            const int sub = nitems <= nth ? rt / nitems : 0;
+            if (sub >= R) return;
+            const uint64_t gam = 0x9E3779B97F4A7C15ull;
+            const uint64_t inc = (uint64_t)gridDim.x * (uint64_t)CT * gam;  // one tile of this CTA
+            uint64_t st[kIpt];
+            int o0[kIpt], o1[kIpt], c0[kIpt];
+            bool on[kIpt];
+#pragma unroll
+            for (int i = 0; i < kIpt; ++i) {
+                const int item = nitems <= nth ? rt - sub * nitems : rt + i * nth;
+                on[i] = item < nitems && (i == 0 || nitems > nth);
+                const int k = on[i] ? item / npmax : 0;
+                const int jj = on[i] ? item - k * npmax : 0;
+                o0[i] = omega_idx(2 * jj, k, NT);
+                o1[i] = omega_idx(2 * jj + 1, k, NT);
+                c0[i] = 2 * jj;
+                const uint64_t p0 = ((a.D + (uint64_t)a.col_off +
+                                      ((uint64_t)blockIdx.x + (uint64_t)sub * gridDim.x) * CT +
+                                      (uint64_t)a.rows_glob * (uint64_t)k) >> 1) + (uint64_t)jj;
+                st[i] = a.seed + (2ull * p0 + 1ull) * gam;
+            }
+            const int64_t full_tiles = a.ncols / CT;  // tiles t < full_tiles have all CT columns
+            for (int j = sub; j < nl; j += G) {
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u) {
+                    const int jt = j + u * R;
+                    if (jt < nl) mbar_wait(&empty_o[jt % nob], ((jt / nob) & 1) ^ 1);
+                }
+                double z[kIlp][kIpt][2];
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u)
+#pragma unroll
+                    for (int i = 0; i < kIpt; ++i) {
+#ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
+                        z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
+#else
+                        gauss_pair_state(st[i] + (uint64_t)(u * R) * inc, *tabs, z[u][i][0], z[u][i][1]);
+#endif
+                    }
+#pragma unroll
+                for (int i = 0; i < kIpt; ++i) st[i] += (uint64_t)G * inc;
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u) {
+                    const int jt = j + u * R;
+                    if (jt >= nl) break;
+                    double* O = omega + (jt % nob) * omega_elems;
+                    const int64_t t = blockIdx.x + (int64_t)jt * gridDim.x;
+                    const int64_t ncol = t < full_tiles ? CT : a.ncols - t * CT;
+#pragma unroll
+                    for (int i = 0; i < kIpt; ++i) {
+                        if (!on[i]) continue;
+                        O[o0[i]] = c0[i] < ncol ? z[u][i][0] : 0.0;
+                        O[o1[i]] = c0[i] + 1 < ncol ? z[u][i][1] : 0.0;
+                    }
+                    mbar_arrive(&full_o[jt % nob]);
+                }
+            }
+            return;
+        }
         // kIlp tiles per iteration: each thread runs kIlp independent Box-Muller chains (one per
         // tile), which hides the chains' fp64 latency behind each other (the FP64 datapath is
         // shared with the consumers' DMMAs, which stretches every dependent step)
@@ -125,7 +202,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             const int ntl = (int)min((int64_t)kIlp, (int64_t)(nl - j));
 #pragma unroll
             for (int u = 0; u < kIlp; ++u)
-                if (u < ntl) mbar_wait(&empty_o[(j + u) % kOB], (((j + u) / kOB) & 1) ^ 1);
+                if (u < ntl) mbar_wait(&empty_o[(j + u) % nob], (((j + u) / nob) & 1) ^ 1);
             for (int it = rt; it < nitems; it += kRng * 32) {
                 const int k = it / npmax;
                 const int jj = it - k * npmax;
@@ -146,7 +223,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                     if (!live[u]) continue;
                     const int64_t c0 = (blockIdx.x + (int64_t)(j + u) * gridDim.x) * CT;
                     const int64_t ncol = imin64(CT, a.ncols - c0);
-                    double* O = omega + ((j + u) % kOB) * omega_elems;
+                    double* O = omega + ((j + u) % nob) * omega_elems;
                     const int64_t c = cc[u];
                     if (c >= 0 && c < CT) O[omega_idx((int)c, k, NT)] = c < ncol ? z[u][0] : 0.0;
                     if (c + 1 >= 0 && c + 1 < CT) O[omega_idx((int)c + 1, k, NT)] = c + 1 < ncol ? z[u][1] : 0.0;
@@ -154,7 +231,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             }
 #pragma unroll
             for (int u = 0; u < kIlp; ++u)
-                if (u < ntl) mbar_arrive(&full_o[(j + u) % kOB]);
+                if (u < ntl) mbar_arrive(&full_o[(j + u) % nob]);
         }
         return;
     }
@@ -171,32 +248,40 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
 #pragma unroll
         for (int jn = 0; jn < NT; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
     const int q = lane >> 2, r = lane & 3;
-    for (int j = 0; j < nl; ++j) {
-        const int s = j % kStages;
-        const int b = j % kOB;
-        mbar_wait(&full_x[s], (j / kStages) & 1);
-        mbar_wait(&full_o[b], (j / kOB) & 1);
+    const int ksteps = CT / 4;
+    for (int j = 0, s = 0, ph = 0; j < nl; ++j) {
+        const int b = j % nob;
+        mbar_wait(&full_x[s], ph);
+        mbar_wait(&full_o[b], (j / nob) & 1);
         const double* X = stages + s * stage_elems + r * dim + q + 8 * mt0;
-        const double* O = omega + b * omega_elems;
+        const double* O = omega + b * omega_elems + lane;
 #pragma unroll
         for (int i4 = 0; i4 < 4; ++i4) {  // k-steps t = tg, tg + 4, ... < CT / 4 <= 16
             const int t = tg + 4 * i4;
-            if (t >= CT / 4) break;
-            double bv[NT];
+            if (t >= ksteps) break;
+            // all fragments of the k-step first, then the MMAs: one load latency per k-step.
+            // Row tiles past my_mt read the zeroed stage pad / the next columns (finite values)
+            // into accumulators the reduction never reads.
+            double bv[NT], av[MTW];
 #pragma unroll
-            for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
+            for (int jn = 0; jn < NT; ++jn) bv[jn] = O[(t * NT + jn) << 5];
             const double* xrow = X + 4 * t * dim;
 #pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-                if (mt < my_mt) {
-                    const double av = xrow[8 * mt];
+            for (int mt = 0; mt < MTW; ++mt) av[mt] = xrow[8 * mt];
 #pragma unroll
-                    for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av, bv[jn]);
+            for (int mt = 0; mt < MTW; ++mt)
+#pragma unroll
+                for (int jn = 0; jn < NT; ++jn) {
+#ifdef TRG_SK_NOMMA  // measurement only: the tensor work removed
+                    acc[mt][jn][0] += av[mt] * bv[jn];
+#else
+                    dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
+#endif
                 }
-            }
         }
         mbar_arrive(&empty_x[s]);
         mbar_arrive(&empty_o[b]);
+        if (++s == nstg) s = 0, ph ^= 1;
     }
     // fixed-order reduction over the 4 k-step groups through (consumed) stage 0;
     // the two halves of a group write disjoint rows
@@ -605,7 +690,6 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
     }
     for (int j = 0; j < nl; ++j) {
         const int s = j % kStages;
-        if (j == nl - 1) griddep_launch_dependents();  // last tile: let the next kernel's launch overlap
         mbar_wait(&full_x[s], (j / kStages) & 1);
         // B fragment: X^T(d = 4t + r, row = 8 nt + q) = X[row][d]
         const double* x0 = stages + s * stage_elems + (16 * warp + q) * dim + r;
@@ -657,15 +741,51 @@ constexpr size_t kSmemBudget = 220 * 1024;
 }  // namespace
 
 // ---------------------------------------------------------------- sketch
+// Shared-memory plan of the mode-0 sketch: CT columns per tile, as many X stages as fit (the
+// bytes in flight per SM set the HBM rate), and enough Omega buffers for the generators to
+// fill one group of tiles while the consumers read the previous one.
+struct SkPlan {
+    int CT, nstg, nob, pad;
+    size_t smem;
+};
+
+// row tiles per consumer warp (two halves of ceil(dim / 8) tiles), rounded up to an instantiation
+int sk_mtw(int64_t dim) {
+    const int mtw = (int)(((dim + 7) / 8 + 1) / 2);
+    return mtw <= 2 ? 2 : mtw <= 4 ? 4 : mtw <= 7 ? 7 : 8;
+}
+
+// the unpredicated row tiles of the second half reach row 16 MTW - 1 of the stage's last column
+int sk_pad(int64_t dim) {
+    const int over = 16 * sk_mtw(dim) - (int)dim;
+    return std::max(8, (over + 8 + 1) & ~1);
+}
+
+SkPlan sk_plan(int64_t dim, int K) {
+    SkPlan p{};
+    static const int ct_env = [] {
+        const char* e = getenv("TRG_SK_CT");
+        return e ? atoi(e) : 0;
+    }();
+    p.CT = ct_env > 0 ? ct_env : (dim <= 112 ? 64 : 32);
+    const int NT = nt_for(K);
+    const int nitems = K * (p.CT / 2);
+    const int R = nitems <= kRng * 32 ? std::max(1, (kRng * 32) / nitems) : 1;  // tiles per generator round
+    p.nob = std::min(kMaxOB, std::max(4, 2 * R * kIlp));
+    p.pad = sk_pad(dim);
+    const size_t stage = ((size_t)p.CT * dim + p.pad) * 8;
+    const size_t fixed = (size_t)p.nob * p.CT * NT * 8 * 8 + sizeof(GaussTables) + kBarBytes;
+    p.nstg = fixed < kSmemBudget ? (int)std::min<size_t>(kMaxStg, (kSmemBudget - fixed) / stage) : 0;
+    p.smem = fixed + (size_t)p.nstg * stage;
+    return p;
+}
+
 bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
     if (dtype != F64 || left != 1 || (dim & 1) || K > 64 || dim > 128) return false;
-    // register budget at 17 warps/SM: (row tiles per warp) x (8-column groups) accumulators
+    // register budget at 25 warps/SM: (row tiles per warp) x (8-column groups) accumulators
     const int mtw = (int)((dim + 7) / 8 + 1) / 2;
     if (nt_for(K) > 4 || (nt_for(K) == 4 && mtw > 4)) return false;
-    const int CT = dim <= 112 ? 64 : 32;
-    const size_t smem =
-        (kStages * (size_t)(CT * dim + kPad) + kOB * (size_t)CT * nt_for(K) * 8) * 8 + sizeof(GaussTables) + kBarBytes;
-    return smem <= kSmemBudget;
+    return sk_plan(dim, K).nstg >= 2;
 }
 
 void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
@@ -675,7 +795,11 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.dim = p.dim;
     a.ncols = p.left * p.right;
     a.K = p.K;
-    a.CT = p.dim <= 112 ? 64 : 32;
+    const SkPlan pl = sk_plan(p.dim, p.K);
+    a.CT = pl.CT;
+    a.nstg = pl.nstg;
+    a.nob = pl.nob;
+    a.pad = pl.pad;
     a.ntiles = (a.ncols + a.CT - 1) / a.CT;
     a.mtiles = (int)((p.dim + 7) / 8);
     a.rows_glob = p.rows_glob;
@@ -686,8 +810,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.gt = gauss_tables(s);
     const int NT = nt_for(p.K);
     const int mtw = (a.mtiles + 1) / 2;  // row tiles per consumer warp (two halves)
-    const size_t smem =
-        (kStages * (size_t)(a.CT * a.dim + kPad) + kOB * (size_t)a.CT * NT * 8) * 8 + sizeof(GaussTables) + kBarBytes;
+    const size_t smem = pl.smem;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     *grid_out = grid;
     const int threads = (kSkCons + kRng + 1) * 32;
@@ -714,7 +837,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     }
 #undef TRG_SK_NT
 #undef TRG_SK
-    launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
+    if (y) launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
 }
 
 // ---------------------------------------------------------------- shrink
