@@ -761,24 +761,17 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
             if (!y_ready[n]) sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n]);
+            qr(n);
             if (!pre_started) {
                 // Omega_m of every later slab-kernel mode depends only on shapes and the seed:
-                // generate them on the side stream while this mode's QR (one SM) and
-                // shrink (HBM-bound) run on the main stream
+                // generate them on the side stream once this mode's QR is done, next to its
+                // shrink (HBM-bound, one CTA per SM with room to spare), not next to the QR or
+                // the sketch, which it would slow down
                 pre_started = true;
                 const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
                 schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre);
             }
-            qr(n);
-            if (n == first_proj) {
-                // join the side stream once, here, rather than before every later sketch: each
-                // cross-stream wait would cut a programmatic-dependent-launch edge of the chain
-                for (auto& po : pre)
-                    if (po.ready) {
-                        CK(cudaStreamWaitEvent(ctx->stream, po.ready, 0));
-                        po.joined = true;
-                    }
-            }
+            const bool join_after_shrink = n == first_proj;
             void* out = nullptr;
             const bool escape = n == last_proj;  // the last shrink writes P itself
             // K3: fuse this shrink with the next mode's sketch while P^(1) tiles are on chip
@@ -817,6 +810,15 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 release_owned();
                 owned = out;
                 owned_arena = !escape;
+            }
+            if (join_after_shrink) {
+                // join the side stream once, here, rather than before every later sketch: each
+                // cross-stream wait cuts a programmatic-dependent-launch edge of the chain
+                for (auto& po : pre)
+                    if (po.ready) {
+                        CK(cudaStreamWaitEvent(ctx->stream, po.ready, 0));
+                        po.joined = true;
+                    }
             }
             if (n == N - 1) ctx->allreduce(out, (size_t)(prod(shape, 0, n) * Kn), cdt);
             cur = out;

@@ -230,6 +230,11 @@ __global__ void k_gauss_tables(GaussTables* t) {
         sincospi(2.0 * (i + 0.5) / 256.0, &sn, &cs);
         t->sct[i] = make_double2(sn, cs);
     }
+    if (i < 64) {
+        const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+        const double ef = (double)(i - 53);
+        t->elog[i] = make_double2(ef * ln2_hi, ef * ln2_lo);
+    }
 }
 
 // the same table-driven generator the streaming kernels use, so the exported

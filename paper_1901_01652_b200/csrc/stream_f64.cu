@@ -15,6 +15,7 @@
 // straight into MMA-fragment order while the MMAs run. fp64 is kept
 // end to end because the reference is fp64 and the parity bound is 1e-10.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -29,12 +30,19 @@ namespace {
 
 constexpr int kStages = 3;
 constexpr int kCons = 4;    // consumer warps (shrink)
-constexpr int kSkCons = 8;  // consumer warps (sketch): 2 per SM sub-partition keep the DMMA pipe fed
+#ifndef TRG_SK_CONS
+#define TRG_SK_CONS 12
+#endif
+// consumer warps (sketch): kSkCons / 4 per SM sub-partition issue DMMAs; warp w takes the k-steps
+// (w & 3) + 4 i of every tile over row-tile group w >> 2 of kSkGrp
+constexpr int kSkCons = TRG_SK_CONS;
+constexpr int kSkGrp = kSkCons / 4;
+static_assert(kSkCons % 4 == 0 && kSkGrp >= 1 && kSkGrp <= 4, "sketch consumers: 4, 8, 12 or 16 warps");
 #ifndef TRG_SK_RNG
 #define TRG_SK_RNG 8
 #endif
 #ifndef TRG_SK_ILP
-#define TRG_SK_ILP 2
+#define TRG_SK_ILP 1
 #endif
 constexpr int kRng = TRG_SK_RNG;  // Omega generator warps (sketch): one Box-Muller pair per thread per tile
 constexpr int kIlp = TRG_SK_ILP;  // independent pairs per generator thread per iteration
@@ -58,14 +66,52 @@ struct SkArgs {
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
 
+#ifdef TRG_SK_PROF  // development: cycle breakdown of CTA 0's generator warp 0 and consumer warp 0
+__device__ unsigned long long g_sk_prof[16];
+#define SK_T(v) long long v = clock64()
+#define SK_ADD(i, d) \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) atomicAdd(&g_sk_prof[i], (unsigned long long)(d))
+#else
+#define SK_T(v)
+#define SK_ADD(i, d)
+#endif
+
 __device__ __forceinline__ int omega_idx(int c, int k, int NT) {
     return (((c >> 2) * NT + (k >> 3)) << 5) + (c & 3) + ((k & 7) << 2);
+}
+
+// One tile's k-steps t = tg, tg + 4, ... (< CT / 4 <= 16) of a consumer warp over NMT row tiles:
+// all fragments of a k-step are loaded first, then its MMAs, so each k-step pays one load latency.
+template <int NMT, int MTW, int NT>
+__device__ __forceinline__ void sk_consume(double (&acc)[MTW][NT][2], const double* X, const double* O, int tg,
+                                           int ksteps, int64_t dim) {
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4) {
+        const int t = tg + 4 * i4;
+        if (t >= ksteps) break;
+        double bv[NT], av[NMT];
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) bv[jn] = O[(t * NT + jn) << 5];
+        const double* xrow = X + 4 * t * dim;
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt) av[mt] = xrow[8 * mt];
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt)
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) {
+#ifdef TRG_SK_NOMMA  // measurement only: the tensor work removed
+                acc[mt][jn][0] += av[mt] * bv[jn];
+#else
+                dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
+#endif
+            }
+    }
 }
 
 template <int MTW, int NT>
 __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(SkArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    griddep_wait();
+    SK_T(k0);
     const int CT = a.CT;
     const int64_t dim = a.dim;
     const int nstg = a.nstg, nob = a.nob;
@@ -106,6 +152,11 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
         fence_mbar_init();
     }
     __syncthreads();
+    // everything above is independent of the preceding kernel (PDL): the test-matrix tables were
+    // built once, long before
+    griddep_wait();
+    SK_T(k1);
+    if (threadIdx.x == 0) SK_ADD(5, k1 - k0);
 
     if (warp == kSkCons + kRng) {
         // ---------------- producer: TMA bulk copies of CT whole columns
@@ -135,7 +186,8 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             // pair index advances by gridDim.x * CT / 2, i.e. the SplitMix64 state by
             // gridDim.x * CT * gamma, so no per-tile index arithmetic is left in the loop.
             constexpr int nth = kRng * 32;
-            const int R = nitems <= nth ? nth / nitems : 1, G = R * kIlp;
+            // R <= kMaxOB / kIlp keeps a group of G tiles within the Omega buffers (sk_plan)
+            const int R = nitems <= nth ? min(nth / nitems, kMaxOB / kIlp) : 1, G = R * kIlp;
             const int sub = nitems <= nth ? rt / nitems : 0;
             if (sub >= R) return;
             const uint64_t gam = 0x9E3779B97F4A7C15ull;
@@ -158,12 +210,22 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                 st[i] = a.seed + (2ull * p0 + 1ull) * gam;
             }
             const int64_t full_tiles = a.ncols / CT;  // tiles t < full_tiles have all CT columns
-            for (int j = sub; j < nl; j += G) {
+            // local tiles jt < jfull are full; buffer index and phase of tile j + u R advance by G
+            const int64_t jf = (full_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+            const int jfull = jf > 0 ? (int)jf : 0;
+            const uint64_t incR = (uint64_t)R * inc, incG = (uint64_t)G * inc;
+            int bix[kIlp], bph[kIlp];
 #pragma unroll
-                for (int u = 0; u < kIlp; ++u) {
-                    const int jt = j + u * R;
-                    if (jt < nl) mbar_wait(&empty_o[jt % nob], ((jt / nob) & 1) ^ 1);
-                }
+            for (int u = 0; u < kIlp; ++u) {
+                bix[u] = (sub + u * R) % nob;
+                bph[u] = ((sub + u * R) / nob) & 1;
+            }
+            for (int j = sub; j < nl; j += G) {
+                SK_T(t0);
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u)
+                    if (j + u * R < nl) mbar_wait(&empty_o[bix[u]], bph[u] ^ 1);
+                SK_T(t1);
                 double z[kIlp][kIpt][2];
 #pragma unroll
                 for (int u = 0; u < kIlp; ++u)
@@ -172,25 +234,43 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
 #ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
                         z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
 #else
-                        gauss_pair_state(st[i] + (uint64_t)(u * R) * inc, *tabs, z[u][i][0], z[u][i][1]);
+                        gauss_pair_state(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0], z[u][i][1]);
 #endif
                     }
 #pragma unroll
-                for (int i = 0; i < kIpt; ++i) st[i] += (uint64_t)G * inc;
+                for (int i = 0; i < kIpt; ++i) st[i] += incG;
 #pragma unroll
                 for (int u = 0; u < kIlp; ++u) {
                     const int jt = j + u * R;
                     if (jt >= nl) break;
-                    double* O = omega + (jt % nob) * omega_elems;
-                    const int64_t t = blockIdx.x + (int64_t)jt * gridDim.x;
-                    const int64_t ncol = t < full_tiles ? CT : a.ncols - t * CT;
+                    double* O = omega + bix[u] * omega_elems;
+                    if (jt < jfull) {
 #pragma unroll
-                    for (int i = 0; i < kIpt; ++i) {
-                        if (!on[i]) continue;
-                        O[o0[i]] = c0[i] < ncol ? z[u][i][0] : 0.0;
-                        O[o1[i]] = c0[i] + 1 < ncol ? z[u][i][1] : 0.0;
+                        for (int i = 0; i < kIpt; ++i)
+                            if (on[i]) {
+                                O[o0[i]] = z[u][i][0];
+                                O[o1[i]] = z[u][i][1];
+                            }
+                    } else {
+                        const int64_t ncol = a.ncols - (blockIdx.x + (int64_t)jt * gridDim.x) * CT;
+#pragma unroll
+                        for (int i = 0; i < kIpt; ++i)
+                            if (on[i]) {
+                                O[o0[i]] = c0[i] < ncol ? z[u][i][0] : 0.0;
+                                O[o1[i]] = c0[i] + 1 < ncol ? z[u][i][1] : 0.0;
+                            }
                     }
-                    mbar_arrive(&full_o[jt % nob]);
+                    mbar_arrive(&full_o[bix[u]]);
+                    bix[u] += G;
+                    if (bix[u] >= nob) {
+                        bix[u] -= nob;
+                        bph[u] ^= 1;
+                    }
+                }
+                SK_T(t2);
+                if (warp == kSkCons) {
+                    SK_ADD(0, t1 - t0);
+                    SK_ADD(1, t2 - t1);
                 }
             }
             return;
@@ -236,12 +316,13 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
         return;
     }
     // ---------------- consumer warps: Y(d, k) += sum_c X(d, c) Omega(c, k)
-    // Warp w takes k-steps t = (w & 3), (w & 3) + 4, ... of every tile and the
-    // row-tile half (w >> 2) (MTW <= 8 row tiles of 8), so two warps per SM
-    // sub-partition issue DMMAs and the accumulators stay at 4*MTW doubles.
-    const int tg = warp & 3, half = warp >> 2;
-    const int mt0 = half * MTW;
-    const int my_mt = min(MTW, a.mtiles - mt0);
+    // Warp w takes k-steps t = (w & 3), (w & 3) + 4, ... of every tile and row-tile group w >> 2:
+    // the mtiles row tiles split as evenly as possible (the first mtiles % kSkGrp groups take one
+    // more), MTW = the larger share, so the accumulators stay at 4 MTW doubles.
+    const int tg = warp & 3, grp = warp >> 2;
+    const int mt_base = a.mtiles / kSkGrp, mt_extra = a.mtiles % kSkGrp;
+    const int mt0 = grp * mt_base + min(grp, mt_extra);
+    const int my_mt = mt_base + (grp < mt_extra ? 1 : 0);
     double acc[MTW][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MTW; ++mt)
@@ -251,40 +332,35 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     const int ksteps = CT / 4;
     for (int j = 0, s = 0, ph = 0; j < nl; ++j) {
         const int b = j % nob;
+        SK_T(c0);
         mbar_wait(&full_x[s], ph);
+        SK_T(c1);
         mbar_wait(&full_o[b], (j / nob) & 1);
+        SK_T(c2);
         const double* X = stages + s * stage_elems + r * dim + q + 8 * mt0;
         const double* O = omega + b * omega_elems + lane;
-#pragma unroll
-        for (int i4 = 0; i4 < 4; ++i4) {  // k-steps t = tg, tg + 4, ... < CT / 4 <= 16
-            const int t = tg + 4 * i4;
-            if (t >= ksteps) break;
-            // all fragments of the k-step first, then the MMAs: one load latency per k-step.
-            // Row tiles past my_mt read the zeroed stage pad / the next columns (finite values)
-            // into accumulators the reduction never reads.
-            double bv[NT], av[MTW];
-#pragma unroll
-            for (int jn = 0; jn < NT; ++jn) bv[jn] = O[(t * NT + jn) << 5];
-            const double* xrow = X + 4 * t * dim;
-#pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) av[mt] = xrow[8 * mt];
-#pragma unroll
-            for (int mt = 0; mt < MTW; ++mt)
-#pragma unroll
-                for (int jn = 0; jn < NT; ++jn) {
-#ifdef TRG_SK_NOMMA  // measurement only: the tensor work removed
-                    acc[mt][jn][0] += av[mt] * bv[jn];
-#else
-                    dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
-#endif
-                }
-        }
+        // groups past mt_extra run one tile fewer (compile-time counts, no predication); any
+        // other shortfall computes padded tiles the reduction never reads
+        if (my_mt == MTW - 1 && MTW > 1)
+            sk_consume<(MTW > 1 ? MTW - 1 : 1), MTW, NT>(acc, X, O, tg, ksteps, dim);
+        else
+            sk_consume<MTW, MTW, NT>(acc, X, O, tg, ksteps, dim);
         mbar_arrive(&empty_x[s]);
         mbar_arrive(&empty_o[b]);
         if (++s == nstg) s = 0, ph ^= 1;
+        SK_T(c3);
+        if (warp == 0) {
+            if (j == 0) SK_ADD(8, c0 - k0);
+            if (j == nl - 1) SK_ADD(9, c3 - k0);
+            SK_ADD(2, c1 - c0);
+            SK_ADD(3, c2 - c1);
+            SK_ADD(4, c3 - c2);
+        }
     }
     // fixed-order reduction over the 4 k-step groups through (consumed) stage 0;
     // the two halves of a group write disjoint rows
+    SK_T(e0);
+    if (threadIdx.x == 0) SK_ADD(7, e0 - k0);
     griddep_launch_dependents();
     asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
     double* red = stages;
@@ -311,6 +387,8 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
         const int d = e - k * (int)dim;
         out[d + dim * k] = red[d + ld * k];
     }
+    SK_T(k3);
+    if (threadIdx.x == 0) SK_ADD(6, k3 - k0);
 }
 
 struct TtmArgs {
@@ -749,15 +827,16 @@ struct SkPlan {
     size_t smem;
 };
 
-// row tiles per consumer warp (two halves of ceil(dim / 8) tiles), rounded up to an instantiation
+// row tiles per consumer warp: the larger share of ceil(dim / 8) tiles over kSkGrp groups
 int sk_mtw(int64_t dim) {
-    const int mtw = (int)(((dim + 7) / 8 + 1) / 2);
-    return mtw <= 2 ? 2 : mtw <= 4 ? 4 : mtw <= 7 ? 7 : 8;
+    const int mt = (int)((dim + 7) / 8);
+    return (mt + kSkGrp - 1) / kSkGrp;
 }
 
-// the unpredicated row tiles of the second half reach row 16 MTW - 1 of the stage's last column
+// zeroed doubles after each stage: the row tiles of the last group reach row 8 kSkGrp MTW - 1 at
+// most (an uneven split never overruns; the slack is for safety)
 int sk_pad(int64_t dim) {
-    const int over = 16 * sk_mtw(dim) - (int)dim;
+    const int over = 8 * kSkGrp * sk_mtw(dim) - (int)dim;
     return std::max(8, (over + 8 + 1) & ~1);
 }
 
@@ -770,7 +849,7 @@ SkPlan sk_plan(int64_t dim, int K) {
     p.CT = ct_env > 0 ? ct_env : (dim <= 112 ? 64 : 32);
     const int NT = nt_for(K);
     const int nitems = K * (p.CT / 2);
-    const int R = nitems <= kRng * 32 ? std::max(1, (kRng * 32) / nitems) : 1;  // tiles per generator round
+    const int R = nitems <= kRng * 32 ? std::max(1, std::min((kRng * 32) / nitems, kMaxOB / kIlp)) : 1;  // tiles per generator round
     p.nob = std::min(kMaxOB, std::max(4, 2 * R * kIlp));
     p.pad = sk_pad(dim);
     const size_t stage = ((size_t)p.CT * dim + p.pad) * 8;
@@ -782,8 +861,8 @@ SkPlan sk_plan(int64_t dim, int K) {
 
 bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
     if (dtype != F64 || left != 1 || (dim & 1) || K > 64 || dim > 128) return false;
-    // register budget at 25 warps/SM: (row tiles per warp) x (8-column groups) accumulators
-    const int mtw = (int)((dim + 7) / 8 + 1) / 2;
+    // register budget: (row tiles per warp) x (8-column groups) accumulators
+    const int mtw = sk_mtw(dim);
     if (nt_for(K) > 4 || (nt_for(K) == 4 && mtw > 4)) return false;
     return sk_plan(dim, K).nstg >= 2;
 }
@@ -809,7 +888,7 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.partial = partial;
     a.gt = gauss_tables(s);
     const int NT = nt_for(p.K);
-    const int mtw = (a.mtiles + 1) / 2;  // row tiles per consumer warp (two halves)
+    const int mtw = sk_mtw(p.dim);
     const size_t smem = pl.smem;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     *grid_out = grid;
@@ -823,21 +902,32 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     switch (NT) {                        \
         case 1: TRG_SK(MTW, 1); break;   \
         case 2: TRG_SK(MTW, 2); break;   \
-        case 4: TRG_SK(MTW, 4); break;   \
-        default: TRG_SK(MTW, 8); break;  \
+        default: TRG_SK(MTW, 4); break;  \
     }
-    if (mtw <= 2) {
-        TRG_SK_NT(2)
-    } else if (mtw <= 4) {
-        TRG_SK_NT(4)
-    } else if (mtw <= 7) {
-        TRG_SK_NT(7)
-    } else {
-        TRG_SK_NT(8)
+    static_assert(16 / kSkGrp <= 8, "row-tile instantiations");
+    switch (mtw) {
+        case 1: TRG_SK_NT(1) break;
+        case 2: TRG_SK_NT(2) break;
+        case 3: TRG_SK_NT(3) break;
+        case 4: TRG_SK_NT(4) break;
+        case 5: TRG_SK_NT(5) break;
+        case 6: TRG_SK_NT(6) break;
+        case 7: TRG_SK_NT(7) break;
+        default: TRG_SK_NT(8) break;
     }
 #undef TRG_SK_NT
 #undef TRG_SK
     if (y) launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
+#ifdef TRG_SK_PROF
+    unsigned long long h[16];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_sk_prof, sizeof(h));
+    fprintf(stderr, "sk_prof gen: wait_empty %llu compute %llu | cons: wait_x %llu wait_o %llu mma %llu | prologue %llu loop_end %llu total %llu\n", h[0], h[1],
+            h[2], h[3], h[4], h[5], h[7], h[6]);
+    fprintf(stderr, "sk_prof first_iter_start %llu last_iter_end %llu\n", h[8], h[9]);
+    static const unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_sk_prof, z, sizeof(z));
+#endif
 }
 
 // ---------------------------------------------------------------- shrink
