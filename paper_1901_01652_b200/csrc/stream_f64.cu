@@ -135,7 +135,10 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     const bool odd = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) != 0;
     const int npmax = odd ? CT / 2 + 1 : CT / 2;
     const int nitems = a.K * npmax;
-    const bool fast = !odd && nitems <= kIpt * kRng * 32;
+    // fast-path slots: a warp's 32 slots cover 8 columns x 4 row pairs of one 32-row block of the
+    // B-fragment layout, so its 16-byte stores of (row 2jj, row 2jj + 1) hit distinct banks
+    const int nslots = ((a.K + 7) / 8 * 8) * ((npmax + 3) / 4 * 4);
+    const bool fast = !odd && nslots <= kIpt * kRng * 32;
 
     for (int i = tid; i < nstg * stage_elems; i += blockDim.x) stages[i] = 0.0;
     for (int i = tid; i < nob * omega_elems; i += blockDim.x) omega[i] = 0.0;
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             mbar_init(&empty_x[s], kSkCons * 32);
         }
         for (int b = 0; b < nob; ++b) {
-            mbar_init(&full_o[b], fast ? min(nitems, kRng * 32) : kRng * 32);
+            mbar_init(&full_o[b], fast ? min(nslots, kRng * 32) : kRng * 32);
             mbar_init(&empty_o[b], kSkCons * 32);
         }
         fence_mbar_init();
@@ -187,22 +190,24 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             // gridDim.x * CT * gamma, so no per-tile index arithmetic is left in the loop.
             constexpr int nth = kRng * 32;
             // R <= kMaxOB / kIlp keeps a group of G tiles within the Omega buffers (sk_plan)
-            const int R = nitems <= nth ? min(nth / nitems, kMaxOB / kIlp) : 1, G = R * kIlp;
-            const int sub = nitems <= nth ? rt / nitems : 0;
+            const int R = nslots <= nth ? min(nth / nslots, kMaxOB / kIlp) : 1, G = R * kIlp;
+            const int sub = nslots <= nth ? rt / nslots : 0;
             if (sub >= R) return;
+            const int KH = (a.K + 7) / 8;
             const uint64_t gam = 0x9E3779B97F4A7C15ull;
             const uint64_t inc = (uint64_t)gridDim.x * (uint64_t)CT * gam;  // one tile of this CTA
             uint64_t st[kIpt];
-            int o0[kIpt], o1[kIpt], c0[kIpt];
+            int o0[kIpt], c0[kIpt];
             bool on[kIpt];
 #pragma unroll
             for (int i = 0; i < kIpt; ++i) {
-                const int item = nitems <= nth ? rt - sub * nitems : rt + i * nth;
-                on[i] = item < nitems && (i == 0 || nitems > nth);
-                const int k = on[i] ? item / npmax : 0;
-                const int jj = on[i] ? item - k * npmax : 0;
-                o0[i] = omega_idx(2 * jj, k, NT);
-                o1[i] = omega_idx(2 * jj + 1, k, NT);
+                const int slot = nslots <= nth ? rt - sub * nslots : rt + i * nth;
+                const int grp = slot >> 5, l = slot & 31;
+                const int kq = 8 * (grp % KH) + (l & 7), jq = 4 * (grp / KH) + (l >> 3);
+                on[i] = slot < nslots && kq < a.K && jq < npmax && (i == 0 || nslots > nth);
+                const int k = on[i] ? kq : 0;
+                const int jj = on[i] ? jq : 0;
+                o0[i] = omega_idx(2 * jj, k, NT);  // row 2jj + 1 is the next double (2jj even)
                 c0[i] = 2 * jj;
                 const uint64_t p0 = ((a.D + (uint64_t)a.col_off +
                                       ((uint64_t)blockIdx.x + (uint64_t)sub * gridDim.x) * CT +
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
 #ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
                         z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
 #else
-                        gauss_pair_state(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0], z[u][i][1]);
+                        gauss_pair_fast(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0], z[u][i][1]);
 #endif
                     }
 #pragma unroll
@@ -247,18 +252,14 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                     if (jt < jfull) {
 #pragma unroll
                         for (int i = 0; i < kIpt; ++i)
-                            if (on[i]) {
-                                O[o0[i]] = z[u][i][0];
-                                O[o1[i]] = z[u][i][1];
-                            }
+                            if (on[i]) *reinterpret_cast<double2*>(O + o0[i]) = make_double2(z[u][i][0], z[u][i][1]);
                     } else {
                         const int64_t ncol = a.ncols - (blockIdx.x + (int64_t)jt * gridDim.x) * CT;
 #pragma unroll
                         for (int i = 0; i < kIpt; ++i)
-                            if (on[i]) {
-                                O[o0[i]] = c0[i] < ncol ? z[u][i][0] : 0.0;
-                                O[o1[i]] = c0[i] + 1 < ncol ? z[u][i][1] : 0.0;
-                            }
+                            if (on[i])
+                                *reinterpret_cast<double2*>(O + o0[i]) =
+                                    make_double2(c0[i] < ncol ? z[u][i][0] : 0.0, c0[i] + 1 < ncol ? z[u][i][1] : 0.0);
                     }
                     mbar_arrive(&full_o[bix[u]]);
                     bix[u] += G;
@@ -848,8 +849,8 @@ SkPlan sk_plan(int64_t dim, int K) {
     }();
     p.CT = ct_env > 0 ? ct_env : (dim <= 112 ? 64 : 32);
     const int NT = nt_for(K);
-    const int nitems = K * (p.CT / 2);
-    const int R = nitems <= kRng * 32 ? std::max(1, std::min((kRng * 32) / nitems, kMaxOB / kIlp)) : 1;  // tiles per generator round
+    const int nslots = ((K + 7) / 8 * 8) * ((p.CT / 2 + 3) / 4 * 4);  // as the kernel's fast path
+    const int R = nslots <= kRng * 32 ? std::max(1, std::min((kRng * 32) / nslots, kMaxOB / kIlp)) : 1;  // tiles per generator round
     p.nob = std::min(kMaxOB, std::max(4, 2 * R * kIlp));
     p.pad = sk_pad(dim);
     const size_t stage = ((size_t)p.CT * dim + p.pad) * 8;
