@@ -108,8 +108,10 @@ void launch_qr(const double* y, int64_t m, int k, double* q, double* work, int* 
 // launch; writes Y and Q. Returns false (nothing launched) when the shape is outside the
 // fused kernel (k > 32 or the staging does not fit), then the caller reduces and calls launch_qr.
 bool qr_fused_ok(int64_t m, int k);
+// ticket: zero-initialised int the reducing CTAs count arrivals on (reset by the last one); null
+// -> a separate reduction kernel. Returns the number of kernels launched.
 int launch_qr_fused(const double* part, int nparts, int64_t m, int k, double* y, double* q, double* work, int* flag,
-                    cudaStream_t s);  // returns the number of kernels launched
+                    int* ticket, cudaStream_t s);
 // Rinv = (upper(Q^T Y))^-1, k x k col-major, so that Q = Y Rinv; *bad set if R is near-singular
 void launch_rinv(const double* q, const double* y, int64_t m, int k, double* rinv, int* bad, cudaStream_t s);
 

@@ -269,7 +269,7 @@ struct trg_sketch {
     std::vector<int64_t> dims, K;
     std::vector<double*> dQ;  // device Q_n (nullptr for skipped modes)
     std::vector<double*> dY;  // device Y_n full rows
-    int* dflags = nullptr;    // N QR-path flags, then (deferred) N near-singular-R flags
+    int* dflags = nullptr;    // N QR-path flags, (deferred) N near-singular-R flags, N QR-reduce tickets
     void* dP = nullptr;       // device P (dtype), full prod K
     bool P_is_view = false;   // P aliases x (no mode projected, unsharded)
     int64_t P_elems = 0;
@@ -702,8 +702,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     if (!sk->ev0) CK(cudaEventCreate(&sk->ev0));
     if (!sk->ev1) CK(cudaEventCreate(&sk->ev1));
     CK(cudaEventRecord(sk->ev0, ctx->stream));
-    sk->dflags = (int*)ctx->alloc(sizeof(int) * 2 * N);
-    CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 2 * N, ctx->stream));
+    sk->dflags = (int*)ctx->alloc(sizeof(int) * 3 * N);  // + N arrival tickets of the fused QR reduce
+    CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 3 * N, ctx->stream));
     sk->x = x;
     sk->seed = seed;
     if (allow_deferred && deferred_eligible(ctx, x, Kin, variant)) {
@@ -743,8 +743,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         if (yparts[n].partial) {
             ctx->launch("qr", [&] {
                 trg::launch_qr_fused(yparts[n].partial, yparts[n].nparts, In, (int)Kn, sk->dY[n], sk->dQ[n], work,
-                                     sk->dflags + n, ctx->stream);
-            }, yparts[n].nparts > 1 ? 2 : 1);
+                                     sk->dflags + n, sk->dflags + 2 * N + n, ctx->stream);
+            });
             ctx->tmp_free(yparts[n].partial);
             yparts[n] = YParts{};
         } else {

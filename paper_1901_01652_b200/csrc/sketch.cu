@@ -234,12 +234,6 @@ __global__ void k_gauss_tables(GaussTables* t) {
         const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
         const double ef = (double)(i - 53);
         t->elog[i] = make_double2(ef * ln2_hi, ef * ln2_lo);
-        t->elog2[i] = make_double2(-2.0 * (ef * ln2_hi), -2.0 * (ef * ln2_lo));
-    }
-    if (i < 128) {
-        const double c = 1.0 + (i + 0.5) / 128.0;
-        t->logt2[i] = make_double2(-2.0 * (1.0 / c), -2.0 * log(c));
-        t->invc[i] = (float)(1.0 / c);
     }
 }
 

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
 #ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
                         z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
 #else
-                        gauss_pair_fast(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0], z[u][i][1]);
+                        gauss_pair_state(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0], z[u][i][1]);
 #endif
                     }
 #pragma unroll
