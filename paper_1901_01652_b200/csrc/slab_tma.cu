@@ -25,6 +25,7 @@
 //
 // One producer thread issues the TMA copies into an S-stage mbarrier ring; each
 // of the 4 consumer warps takes whole units (stage j goes to warp j % 4).
+#include <cstdio>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -39,6 +40,14 @@
 namespace trg {
 
 namespace {
+
+#ifdef TRG_SLAB_PROF  // development: CTA 0 phase timestamps of the slab kernels
+__device__ long long g_slab_prof[2][8];
+#define SLAB_T(kind, i) \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_slab_prof[kind][i] = clock64()
+#else
+#define SLAB_T(kind, i)
+#endif
 
 constexpr int kTCons = 8;    // consumer warps: pairs (w, w + 4) share a unit, two per SM sub-partition
 constexpr int kMaxStg = 8;  // stages (units in flight): 8 measured best (16 was slower on C2/C5 mode 1)
@@ -107,7 +116,9 @@ template <int MTW, int NT>
 __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     k_slab2_sketch_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    SLAB_T(0, 0);
     griddep_wait();
+    SLAB_T(0, 1);
     const int dim = (int)a.dim;
     const int rows_pad = (dim + 7) & ~7;
     const int xbytes = rows_pad * 128;  // multiple of 1024: keeps every stage swizzle-aligned
@@ -160,6 +171,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
         for (int jn = 0; jn < NT; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
+    SLAB_T(0, 2);
     for (int64_t j = pair; j < nl; j += 4) {
         const int s = (int)(j % kStg);
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
@@ -183,33 +195,41 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         __syncwarp();
         mbar_arrive(&empty[s]);
     }
-    // fixed-order sum of the consumer warps' partials through stage 0 (all consumed)
+    // fixed-order sum of the four pairs' partials: every consumer warp parks its accumulators in
+    // its own slice of the (consumed) stages, then one pass adds the pairs in order 0..3
+    SLAB_T(0, 3);
     griddep_launch_dependents();
-    asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
-    double* red = reinterpret_cast<double*>(base);
-    const int ld = 8 * a.mtiles;
-    for (int g = 0; g < 4; ++g) {  // the two halves of a pair write disjoint rows
-        if (pair == g) {
+    const uint32_t rbase = smem_u32(base);
+    const int slice = MTW * NT * 64;  // doubles per warp
+    asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));  // every warp is done with the stages
+    {
+        const uint32_t mine = rbase + 8u * (uint32_t)(warp * slice);
 #pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-                if (mt < my_mt) {
+        for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
-                    for (int jn = 0; jn < NT; ++jn) {
-                        double* p0 = red + (8 * (mt0 + mt) + q) + ld * (8 * jn + 2 * rl);
-                        *p0 = (g == 0 ? 0.0 : *p0) + acc[mt][jn][0];
-                        p0[ld] = (g == 0 ? 0.0 : p0[ld]) + acc[mt][jn][1];
-                    }
-                }
+            for (int jn = 0; jn < NT; ++jn) {
+                sts64(mine + 8u * (uint32_t)(((mt * NT + jn) << 6) + 2 * lane), acc[mt][jn][0]);
+                sts64(mine + 8u * (uint32_t)(((mt * NT + jn) << 6) + 2 * lane + 1), acc[mt][jn][1]);
             }
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
     }
+    asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
+    SLAB_T(0, 5);
+    SLAB_T(0, 6);
     double* outp = a.partial + (int64_t)blockIdx.x * a.dim * a.K;
     for (int e = tid; e < dim * a.K; e += kTCons * 32) {
         const int k = e / dim;
         const int d = e - k * dim;
-        outp[d + a.dim * k] = red[d + ld * k];
+        // row d lives in half h = d / (8 MTW), tile mt, fragment row q; column k in tile jn at
+        // lane 4 q + (k & 7) / 2, element k & 1
+        const int h = d / (8 * MTW), dm = d - 8 * MTW * h;
+        const int mt = dm >> 3, qq = dm & 7, jn = k >> 3, kk = k & 7;
+        const int off = ((mt * NT + jn) << 6) + 2 * (4 * qq + (kk >> 1)) + (kk & 1);
+        double sacc = 0.0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) sacc += lds64(rbase + 8u * (uint32_t)((g + 4 * h) * slice + off));
+        outp[d + a.dim * k] = sacc;
     }
+    SLAB_T(0, 4);
 }
 
 // ------------------------------------------------------------------ shrink
@@ -220,7 +240,9 @@ template <int NT, int TKM>
 __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     k_slab2_ttm_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    SLAB_T(1, 0);
     griddep_wait();
+    SLAB_T(1, 1);
     const int dim = (int)a.dim;
     const int rows_pad = (dim + 7) & ~7;
     const int sbytes = rows_pad * 128;
@@ -271,6 +293,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         return;
     }
     const int pair = warp & 3, mt = warp >> 2;  // pair takes units j = pair (mod 4); mt = 8-row tile of l
+    SLAB_T(1, 2);
     for (int64_t j = pair; j < nl; j += 4) {
         const int s = (int)(j % kStg);
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
@@ -305,6 +328,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
                 }
         }
     }
+    SLAB_T(1, 3);
 }
 
 
@@ -433,6 +457,14 @@ int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_
     }
 #undef TRG_S2
     if (y) launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
+#ifdef TRG_SLAB_PROF
+    long long h[8];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_slab_prof, sizeof(h), 0);
+    fprintf(stderr, "slab_sketch dim=%lld left=%lld right=%lld units/CTA=%lld: wait %lld prologue %lld loop %lld epilogue %lld (sync %lld red %lld write %lld)\n",
+            (long long)p.dim, (long long)p.left, (long long)p.right, (long long)((a.nunits + grid - 1) / grid), h[1] - h[0],
+            h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[3], h[6] - h[5], h[4] - h[6]);
+#endif
     return grid;
 }
 
@@ -469,6 +501,14 @@ void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double*
         if (NT == 1) TRG_T2(1, 32); else TRG_T2(2, 32);
     }
 #undef TRG_T2
+#ifdef TRG_SLAB_PROF
+    long long h[8];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_slab_prof, sizeof(h), sizeof(h));
+    fprintf(stderr, "slab_ttm dim=%lld left=%lld right=%lld units/CTA=%lld: wait %lld prologue %lld loop %lld\n",
+            (long long)p.dim, (long long)p.left, (long long)p.right, (long long)((a.nunits + grid - 1) / grid), h[1] - h[0],
+            h[2] - h[1], h[3] - h[2]);
+#endif
 }
 
 }  // namespace trg
