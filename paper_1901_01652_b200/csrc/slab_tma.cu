@@ -259,16 +259,6 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         for (int i = tid; i < kStg * npad; i += blockDim.x)
             reinterpret_cast<double*>(base + (i / npad) * sbytes)[dim * 16 + i % npad] = 0.0;
     }
-    // B fragments of Q in registers: qb[t][jn] = Q(d = perm_d(t, rl), o = 8 jn + q)
-    double qb[TKM][NT];
-#pragma unroll
-    for (int t = 0; t < TKM; ++t)
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn) {
-            const int d = perm_d(t, rl);
-            const int o = 8 * jn + q;
-            qb[t][jn] = (t < a.Tk && d < dim && o < a.K) ? a.q[d + a.ldq * o] : 0.0;
-        }
     if (tid == 0) {
         for (int s = 0; s < kStg; ++s) {
             mbar_init(&full[s], 1);
@@ -292,6 +282,17 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         }
         return;
     }
+    // B fragments of Q in registers: qb[t][jn] = Q(d = perm_d(t, rl), o = 8 jn + q), loaded while
+    // the producer's first tiles are in flight
+    double qb[TKM][NT];
+#pragma unroll
+    for (int t = 0; t < TKM; ++t)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) {
+            const int d = perm_d(t, rl);
+            const int o = 8 * jn + q;
+            qb[t][jn] = (t < a.Tk && d < dim && o < a.K) ? a.q[d + a.ldq * o] : 0.0;
+        }
     const int pair = warp & 3, mt = warp >> 2;  // pair takes units j = pair (mod 4); mt = 8-row tile of l
     SLAB_T(1, 2);
     for (int64_t j = pair; j < nl; j += 4) {

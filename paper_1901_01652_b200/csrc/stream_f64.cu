@@ -732,16 +732,6 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
     const int q = lane >> 2, r = lane & 3;
 
     for (int i = tid; i < kStages * stage_elems; i += blockDim.x) stages[i] = 0.0;
-    // A fragments of Q^T: qa[mt][t] = Q^T(o = 8 mt + q, d = 4 t + r) = Q(d, o)
-    double qa[MTO][TKM];
-#pragma unroll
-    for (int mt = 0; mt < MTO; ++mt)
-#pragma unroll
-        for (int t = 0; t < TKM; ++t) {
-            const int64_t d = 4 * t + r;
-            const int o = 8 * mt + q;
-            qa[mt][t] = (t < a.Tk && d < dim && o < a.K) ? a.q[d + a.ldq * o] : 0.0;
-        }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_x[s], 1);
@@ -767,6 +757,17 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
         }
         return;
     }
+    // A fragments of Q^T, loaded while the producer's first tiles are in flight:
+    // qa[mt][t] = Q^T(o = 8 mt + q, d = 4 t + r) = Q(d, o)
+    double qa[MTO][TKM];
+#pragma unroll
+    for (int mt = 0; mt < MTO; ++mt)
+#pragma unroll
+        for (int t = 0; t < TKM; ++t) {
+            const int64_t d = 4 * t + r;
+            const int o = 8 * mt + q;
+            qa[mt][t] = (t < a.Tk && d < dim && o < a.K) ? a.q[d + a.ldq * o] : 0.0;
+        }
     for (int j = 0; j < nl; ++j) {
         const int s = j % kStages;
         mbar_wait(&full_x[s], (j / kStages) & 1);
