@@ -112,6 +112,25 @@ __global__ void k_omega_units(int64_t left, int LC, int64_t nunits, int K, int N
 }
 
 // ------------------------------------------------------------------ sketch
+// One unit's 4 k-steps over NMT row tiles: fragments of a k-step first, then its MMAs.
+template <int NMT, int MTW, int NT>
+__device__ __forceinline__ void slab_consume(double (&acc)[MTW][NT][2], const double* X, const double* O, int mt0,
+                                             int q, int rl, int lane) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        double bv[NT], av[NMT];
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
+        const int l = 4 * t + rl;
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt) av[mt] = X[swz(8 * (mt0 + mt) + q, l)];
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt)
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
+    }
+}
+
 template <int MTW, int NT>
 __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     k_slab2_sketch_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
@@ -177,21 +196,11 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
         const double* X = reinterpret_cast<const double*>(base + s * sbytes);
         const double* O = reinterpret_cast<const double*>(base + s * sbytes + xbytes);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            double bv[NT];
-#pragma unroll
-            for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
-            const int l = 4 * t + rl;
-#pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-                if (mt < my_mt) {
-                    const double av = X[swz(8 * (mt0 + mt) + q, l)];
-#pragma unroll
-                    for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av, bv[jn]);
-                }
-            }
-        }
+        // half 1 of an odd row-tile count runs one tile fewer: compile-time counts, no predication
+        if (MTW > 1 && my_mt == MTW - 1)
+            slab_consume<(MTW > 1 ? MTW - 1 : 1), MTW, NT>(acc, X, O, mt0, q, rl, lane);
+        else
+            slab_consume<MTW, MTW, NT>(acc, X, O, mt0, q, rl, lane);
         __syncwarp();
         mbar_arrive(&empty[s]);
     }
@@ -451,10 +460,18 @@ int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_
         set_smem(k_slab2_sketch_f64<MTW, NTV>, smem);                     \
         pdl_launch(k_slab2_sketch_f64<MTW, NTV>, dim3(grid), dim3(threads), smem, s, map, a); \
     } while (0)
-    if (a.mtiles <= 8) {
-        if (NT == 1) TRG_S2(4, 1); else TRG_S2(4, 2);
-    } else {
-        if (NT == 1) TRG_S2(8, 1); else TRG_S2(8, 2);
+    // row tiles per half: ceil(mtiles / 2), exact (half 1 takes the remainder)
+    switch ((a.mtiles + 1) / 2) {
+#define TRG_S2_NT(M) if (NT == 1) TRG_S2(M, 1); else TRG_S2(M, 2); break;
+        case 1: TRG_S2_NT(1)
+        case 2: TRG_S2_NT(2)
+        case 3: TRG_S2_NT(3)
+        case 4: TRG_S2_NT(4)
+        case 5: TRG_S2_NT(5)
+        case 6: TRG_S2_NT(6)
+        case 7: TRG_S2_NT(7)
+        default: TRG_S2_NT(8)
+#undef TRG_S2_NT
     }
 #undef TRG_S2
     if (y) launch_reduce_partials(partial, grid, p.dim * p.K, y, s);
