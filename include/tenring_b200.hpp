@@ -15,6 +15,8 @@
 //   sketch                               sketch.hpp:62-89
 //   back_project                         sketch.hpp:106-122
 //   mode_n_product                       tensor.hpp:193-207
+//   lift_back(sketch_result)             sketch.hpp:93-101
+//   read/write_dten, read/write_trng     io.hpp:84-129, tr_factors.hpp:161-200 (host only)
 //   rse(x, factors)                      solvers.hpp:47-54 of reconstruct_full (tr_factors.hpp:123-137)
 //   rtrals / rtrsvd                      sketch.hpp:154-165
 //   decompose(X, ranks, proj_sizes, method)   north-star entry point
@@ -27,6 +29,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
+#include <fstream>
 #include <iostream>
 #include <memory>
 #include <optional>
@@ -373,6 +377,137 @@ inline TRFactors back_project(const TRFactors& small, trg_sketch* sk, const std:
     std::vector<double> out(static_cast<std::size_t>(total));
     detail::check(trg_back_project(ctx.get(), static_cast<int>(N), K.data(), r.data(), flat.data(), sk, out.data()));
     return TRFactors::from_flat(dims, r, out.data());
+}
+
+/// sketch.hpp:93-101: P x_0 Q_0 x_1 Q_1 ..., computed on the device; a square, exactly-identity
+/// basis is skipped as in the reference.
+inline DenseTensor lift_back(const SketchResult& sk, Context& ctx = default_context()) {
+    const index_t N = sk.projected.order();
+    detail::require(static_cast<index_t>(sk.bases.size()) == N, "lift_back: one basis per mode");
+    std::vector<index_t> dims, K = sk.projected.shape();
+    std::vector<const double*> q;
+    for (index_t n = 0; n < N; ++n) {
+        const Matrix& b = sk.bases[static_cast<std::size_t>(n)];
+        detail::require(b.cols == K[static_cast<std::size_t>(n)], "lift_back: basis columns must equal K_n");
+        dims.push_back(b.rows);
+        q.push_back(b.data());
+    }
+    trg_tensor* out = nullptr;
+    detail::check(trg_lift_back(ctx.get(), static_cast<int>(N), dims.data(), K.data(), sk.projected.data(), q.data(), &out));
+    std::unique_ptr<trg_tensor, int (*)(trg_tensor*)> guard(out, trg_tensor_destroy);
+    DenseTensor r(dims);
+    detail::check(trg_tensor_download(out, r.data()));
+    return r;
+}
+
+// ---- DTEN / TRNG containers (io.hpp:84-129, tr_factors.hpp:161-200) ------------------------
+// DTEN: "DTEN", u32 version 1, u32 order N >= 1, N x u64 extents >= 1, then the f64 values
+// first-index-fastest, all little-endian. TRNG: "TRNG", u32 version 1, u32 count >= 1, then the
+// cores as DTEN records. Round-trips bit-exactly.
+
+/// Malformed or unreadable on-disk data (io.hpp:16-20).
+class format_error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void put_le(std::ostream& os, std::uint64_t v, int bytes) {
+    unsigned char b[8];
+    for (int i = 0; i < bytes; ++i) b[i] = static_cast<unsigned char>((v >> (8 * i)) & 0xFF);
+    os.write(reinterpret_cast<const char*>(b), bytes);
+}
+inline std::uint64_t get_le(std::istream& is, int bytes, const char* what) {
+    unsigned char b[8];
+    is.read(reinterpret_cast<char*>(b), bytes);
+    if (is.gcount() != bytes) throw format_error(std::string("unexpected end of file while reading ") + what);
+    std::uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= static_cast<std::uint64_t>(b[i]) << (8 * i);
+    return v;
+}
+inline void get_magic(std::istream& is, const char* magic, const char* what) {
+    char m[4];
+    is.read(m, 4);
+    if (is.gcount() != 4) throw format_error(std::string("unexpected end of file while reading ") + what + " magic");
+    if (std::memcmp(m, magic, 4) != 0) throw format_error(std::string("not a ") + what + " file (bad magic)");
+}
+}  // namespace detail
+
+inline void write_dten(std::ostream& os, const DenseTensor& t) {
+    os.write("DTEN", 4);
+    detail::put_le(os, 1, 4);
+    detail::put_le(os, static_cast<std::uint64_t>(t.order()), 4);
+    for (index_t d : t.shape()) detail::put_le(os, static_cast<std::uint64_t>(d), 8);
+    for (index_t i = 0; i < t.size(); ++i) {
+        std::uint64_t u;
+        const double v = t[i];
+        std::memcpy(&u, &v, 8);
+        detail::put_le(os, u, 8);
+    }
+    if (!os) throw format_error("I/O error while writing DTEN data");
+}
+
+inline DenseTensor read_dten(std::istream& is) {
+    detail::get_magic(is, "DTEN", "DTEN");
+    const std::uint64_t version = detail::get_le(is, 4, "DTEN version");
+    if (version != 1) throw format_error("unsupported DTEN version " + std::to_string(version));
+    const std::uint64_t order = detail::get_le(is, 4, "DTEN order");
+    if (order == 0) throw format_error("DTEN order must be at least 1");
+    std::vector<index_t> shape;
+    for (std::uint64_t n = 0; n < order; ++n) {
+        const std::uint64_t d = detail::get_le(is, 8, "DTEN extent");
+        if (d == 0) throw format_error("DTEN extents must be positive");
+        shape.push_back(static_cast<index_t>(d));
+    }
+    std::vector<double> data(static_cast<std::size_t>(detail::product(shape)));
+    for (double& x : data) {
+        const std::uint64_t u = detail::get_le(is, 8, "DTEN values");
+        std::memcpy(&x, &u, 8);
+    }
+    return DenseTensor(std::move(shape), std::move(data));
+}
+
+inline void write_trng(std::ostream& os, const TRFactors& f) {
+    os.write("TRNG", 4);
+    detail::put_le(os, 1, 4);
+    detail::put_le(os, static_cast<std::uint64_t>(f.order()), 4);
+    for (index_t n = 0; n < f.order(); ++n) write_dten(os, f.core(n));
+}
+
+inline TRFactors read_trng(std::istream& is) {
+    detail::get_magic(is, "TRNG", "TRNG");
+    const std::uint64_t version = detail::get_le(is, 4, "TRNG version");
+    if (version != 1) throw format_error("unsupported TRNG version " + std::to_string(version));
+    const std::uint64_t n = detail::get_le(is, 4, "TRNG core count");
+    if (n == 0) throw format_error("TRNG must contain at least one core");
+    std::vector<DenseTensor> cores;
+    for (std::uint64_t i = 0; i < n; ++i) cores.push_back(read_dten(is));
+    try {
+        return TRFactors(std::move(cores));
+    } catch (const std::invalid_argument& e) {
+        throw format_error(std::string("TRNG cores are inconsistent: ") + e.what());
+    }
+}
+
+inline void write_dten(const std::string& path, const DenseTensor& t) {
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw format_error("cannot open '" + path + "' for writing");
+    write_dten(os, t);
+}
+inline DenseTensor read_dten(const std::string& path) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw format_error("cannot open '" + path + "' for reading");
+    return read_dten(is);
+}
+inline void write_trng(const std::string& path, const TRFactors& f) {
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw format_error("cannot open '" + path + "' for writing");
+    write_trng(os, f);
+}
+inline TRFactors read_trng(const std::string& path) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw format_error("cannot open '" + path + "' for reading");
+    return read_trng(is);
 }
 
 }  // namespace b200

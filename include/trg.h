@@ -127,6 +127,13 @@ int trg_omega(trg_ctx* ctx, uint64_t seed, uint64_t offset, int64_t rows, int64_
 /* out = x x_mode M (tensor.hpp:193-207); M is m_rows x I_mode col-major. */
 int trg_mode_n_product(trg_ctx* ctx, const trg_tensor* x, int mode, int64_t m_rows, const double* m,
                        trg_tensor** out);
+/* lift_back (sketch.hpp:93-101): P x_0 Q_0 x_1 Q_1 ... (the plain TRP approximation of x), computed
+ * on the device into a new full-size tensor. The sketch-handle form uses the resident P and Q_n; the
+ * host form uploads P (prod K_n) and the bases (I_n x K_n col-major each) and, like the reference,
+ * skips a basis that is square and exactly the identity. Unsharded contexts only. */
+int trg_sketch_lift_back(const trg_sketch* sk, trg_tensor** out);
+int trg_lift_back(trg_ctx* ctx, int order, const int64_t* dims, const int64_t* K, const double* projected,
+                  const double* const* bases, trg_tensor** out);
 /* G_n = Z_n x_2 Q_n (sketch.hpp:106-122); small core n is (R_n, K_n, R_{n+1}). */
 int trg_back_project(trg_ctx* ctx, int order, const int64_t* K, const int64_t* ranks, const double* small_cores,
                      const trg_sketch* sk, double* cores_out);

@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     default_context,
     gaussian_matrix,
     economy_q,
+    lift_back,
     mode_n_product,
     rse,
     rtrals,
@@ -26,3 +27,4 @@ from .api import (  # noqa: F401
     sketch_offsets,
     sketch,
 )
+from .io import FormatError, read_dten, read_trng, write_dten, write_trng  # noqa: F401

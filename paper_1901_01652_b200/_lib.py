@@ -24,7 +24,7 @@ EXPORTS = [
     "trg_tensor_synthesize", "trg_tensor_destroy",
     "trg_sketch_run", "trg_sketch_projected", "trg_sketch_basis", "trg_sketch_y", "trg_sketch_qr_path",
     "trg_sketch_elapsed_ms", "trg_sketch_destroy", "trg_thin_qr", "trg_omega",
-    "trg_mode_n_product", "trg_back_project", "trg_rse",
+    "trg_mode_n_product", "trg_back_project", "trg_rse", "trg_sketch_lift_back", "trg_lift_back",
     "trg_decompose", "trg_decompose_host", "trg_report_ranks", "trg_report_cores_len", "trg_report_cores",
     "trg_report_rse_history", "trg_report_sweeps", "trg_report_timings", "trg_report_projected",
     "trg_report_destroy",

@@ -382,6 +382,45 @@ def mode_n_product(x, mode, m, ctx=None):
     return res
 
 
+def lift_back(sk, ctx=None):
+    """lift_back (sketch.hpp:93-101): P x_0 Q_0 x_1 Q_1 ..., the plain TRP approximation of x.
+
+    A DeviceSketch is lifted from its resident P and Q_n (result: DeviceTensor). A host
+    SketchResult is uploaded and lifted on the device (result: numpy); like the reference, a
+    basis that is square and exactly the identity is skipped.
+    """
+    if isinstance(sk, DeviceSketch):
+        h = ctypes.c_void_p()
+        L.call("trg_sketch_lift_back", sk.handle, ctypes.byref(h))
+        out = DeviceTensor.__new__(DeviceTensor)
+        shape = tuple(sk.dims)
+        out.ctx, out.shape, out._h, out.lo, out.hi = sk.ctx, shape, h, 0, shape[-1]
+        dt = ctypes.c_int()
+        L.call("trg_tensor_info", h, ctypes.byref(dt), None, None, None, None)
+        out.dtype = np.dtype(np.float32 if dt.value == L.TRG_F32 else np.float64)
+        sk.ctx._adopt(out)
+        return out
+    ctx = ctx or default_context()
+    P = np.asarray(sk.projected, dtype=np.float64)
+    bases = [np.asarray(q, dtype=np.float64) for q in sk.bases]
+    if len(bases) != P.ndim or any(q.ndim != 2 or q.shape[1] != P.shape[n] for n, q in enumerate(bases)):
+        raise ValueError("lift_back: bases must be I_n x K_n with K_n the projected extents")
+    dims = [q.shape[0] for q in bases]
+    d, dp = L.i64(dims)
+    k, kp = L.i64(P.shape)
+    flatP = np.ascontiguousarray(P.reshape(-1, order="F"))
+    flats = [np.ascontiguousarray(q.reshape(-1, order="F")) for q in bases]
+    ptrs = (L.c_dp * len(flats))(*[f.ctypes.data_as(L.c_dp) for f in flats])
+    h = ctypes.c_void_p()
+    L.call("trg_lift_back", ctx.handle, ctypes.c_int(len(dims)), dp, kp, flatP.ctypes.data_as(L.c_dp), ptrs,
+           ctypes.byref(h))
+    out = DeviceTensor.__new__(DeviceTensor)
+    out.ctx, out.shape, out.dtype, out._h, out.lo, out.hi = ctx, tuple(dims), np.dtype(np.float64), h, 0, dims[-1]
+    res = out.numpy()
+    out.close()
+    return res
+
+
 def _flat_cores(cores):
     return np.ascontiguousarray(np.concatenate([np.asarray(c, np.float64).reshape(-1, order="F") for c in cores]))
 

@@ -307,7 +307,8 @@ namespace {
 
 int64_t prod(const std::vector<int64_t>& v, size_t b = 0, size_t e = SIZE_MAX) {
     int64_t p = 1;
-    for (size_t i = b; i < std::min(e, v.size()); ++i) p *= v[i];
+    const size_t end = std::min(e, v.size());
+    for (size_t i = b; i < end; ++i) p *= v[i];
     return p;
 }
 
@@ -1534,6 +1535,88 @@ int trg_mode_n_product(trg_ctx* ctx, const trg_tensor* x, int mode, int64_t m_ro
         CK(cudaStreamSynchronize(ctx->stream));
         ctx->dfree(dm);
         *out = o;
+    });
+}
+
+// lift_back (sketch.hpp:93-101): t = P x_0 Q_0 x_1 Q_1 ... on the device, skipping exact
+// identity bases (q == nullptr). P is (dtype) with extents K; the result has extents dims.
+static trg_tensor* lift_back_device(trg_ctx* ctx, int dtype, const std::vector<int64_t>& dims, const std::vector<int64_t>& K,
+                             const void* P, const std::vector<const double*>& q) {
+    require(ctx->world == 1, "lift_back: unsharded tensors only");
+    const int N = (int)dims.size();
+    std::vector<int64_t> cur = K;
+    trg_tensor* out = tensor_new(ctx, dtype, N, dims.data());
+    const size_t es = trg::dtype_size(dtype);
+    int last = -1;
+    for (int n = 0; n < N; ++n)
+        if (q[n]) last = n;
+    if (last < 0) {  // every basis is the identity: t = P
+        CK(cudaMemcpyAsync(out->d, P, es * (size_t)prod(K), cudaMemcpyDeviceToDevice, ctx->stream));
+        return out;
+    }
+    const void* src = P;
+    void* owned = nullptr;
+    for (int n = 0; n <= last; ++n) {
+        if (!q[n]) continue;
+        std::vector<int64_t> nxt = cur;
+        nxt[n] = dims[n];
+        void* dst = n == last ? out->d : ctx->alloc(es * (size_t)prod(nxt));
+        trg::TTMPlan p{};
+        p.dtype = dtype;
+        p.left = prod(cur, 0, n);
+        p.dim = cur[n];
+        p.right = prod(cur, n + 1);
+        p.odim = dims[n];
+        p.m_so = 1;        // M(o = i, d = k) = Q_n[i + I_n k]
+        p.m_sd = dims[n];
+        trg::plan_ttm(p, ctx->num_sms);
+        ctx->launch("lift_back", [&] { trg::launch_ttm(p, src, dst, q[n], ctx->stream); });
+        if (owned) ctx->dfree(owned);
+        owned = n == last ? nullptr : dst;
+        src = dst;
+        cur = nxt;
+    }
+    return out;
+}
+
+int trg_sketch_lift_back(const trg_sketch* csk, trg_tensor** out) {
+    return guard([&] {
+        validate(csk);
+        const trg_sketch* sk = csk;
+        std::vector<const double*> q(sk->dims.size());
+        for (size_t n = 0; n < q.size(); ++n) q[n] = sk->K[n] == sk->dims[n] ? nullptr : sk->dQ[n];
+        *out = lift_back_device(sk->ctx, sk->dtype, sk->dims, sk->K, sk->dP, q);
+        CK(cudaStreamSynchronize(sk->ctx->stream));
+    });
+}
+
+int trg_lift_back(trg_ctx* ctx, int order, const int64_t* dims, const int64_t* K, const double* projected,
+                  const double* const* bases, trg_tensor** out) {
+    return guard([&] {
+        require(ctx && dims && K && projected && bases && out, "lift_back: null argument");
+        require(order >= 1, "lift_back: order must be at least 1");
+        std::vector<int64_t> d(dims, dims + order), k(K, K + order);
+        for (int n = 0; n < order; ++n)
+            require(d[n] >= 1 && k[n] >= 1 && bases[n], "lift_back: extents must be positive, bases non-null");
+        double* dP = (double*)ctx->alloc(sizeof(double) * (size_t)prod(k));
+        CK(cudaMemcpyAsync(dP, projected, sizeof(double) * prod(k), cudaMemcpyHostToDevice, ctx->stream));
+        std::vector<const double*> q(order, nullptr);
+        std::vector<double*> owned;
+        for (int n = 0; n < order; ++n) {
+            // sketch.hpp:98: a square, exactly-identity basis is skipped (no product, bit-exact copy)
+            bool ident = d[n] == k[n];
+            for (int64_t e = 0; ident && e < d[n] * k[n]; ++e)
+                ident = bases[n][e] == ((e % d[n]) == (e / d[n]) ? 1.0 : 0.0);
+            if (ident) continue;
+            double* dq = (double*)ctx->alloc(sizeof(double) * d[n] * k[n]);
+            CK(cudaMemcpyAsync(dq, bases[n], sizeof(double) * d[n] * k[n], cudaMemcpyHostToDevice, ctx->stream));
+            q[n] = dq;
+            owned.push_back(dq);
+        }
+        *out = lift_back_device(ctx, F64, d, k, dP, q);
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->dfree(dP);
+        for (double* p : owned) ctx->dfree(p);
     });
 }
 
