@@ -425,43 +425,61 @@ SolveOut zero_report(const Tensor& x, const std::vector<idx>& ranks) {  // solve
     return o;
 }
 
-// one-sided Jacobi thin SVD, singular values descending (BDCSVD stand-in)
+// one-sided Jacobi thin SVD, singular values descending (BDCSVD stand-in). Sweeps visit the
+// column pairs in round-robin (tournament) order: every round is n/2 disjoint pairs, rotated in
+// parallel, so the 576 x 432 / 1024 x 64 shapes of C5 / C2 use all host cores.
+namespace {
+inline bool jacobi_rotate(double* wp, double* wq, double* vp, double* vq, idx m, idx n) {
+    double al = 0.0, be = 0.0, ga = 0.0;
+    for (idx i = 0; i < m; ++i) {
+        al += wp[i] * wp[i];
+        be += wq[i] * wq[i];
+        ga += wp[i] * wq[i];
+    }
+    if (ga == 0.0 || std::abs(ga) <= 1e-15 * std::sqrt(al * be)) return false;
+    const double zeta = (be - al) / (2.0 * ga);
+    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+    for (idx i = 0; i < m; ++i) {
+        const double x = wp[i], y = wq[i];
+        wp[i] = c * x - sn * y;
+        wq[i] = sn * x + c * y;
+    }
+    for (idx i = 0; i < n; ++i) {
+        const double x = vp[i], y = vq[i];
+        vp[i] = c * x - sn * y;
+        vq[i] = sn * x + c * y;
+    }
+    return true;
+}
+}  // namespace
+
 void svd(const Mat& a, Mat& U, std::vector<double>& s, Mat& V) {
     const bool wide = a.r < a.c;
     Mat W = wide ? transpose(a) : a;
     const idx m = W.r, n = W.c;
     Mat Vw(n, n);
     for (idx i = 0; i < n; ++i) Vw(i, i) = 1.0;
+    // tournament schedule over np = n rounded up to even players (player n is a bye)
+    const idx np = n + (n & 1);
+    std::vector<idx> pos(static_cast<size_t>(np));
+    std::iota(pos.begin(), pos.end(), 0);
+    const bool par = n >= 16 && m * n >= (1 << 14);
     for (int sweep = 0; sweep < 80; ++sweep) {
-        bool rotated = false;
-        for (idx p = 0; p < n - 1; ++p)
-            for (idx q = p + 1; q < n; ++q) {
-                double* wp = W.col(p);
-                double* wq = W.col(q);
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (idx i = 0; i < m; ++i) {
-                    al += wp[i] * wp[i];
-                    be += wq[i] * wq[i];
-                    ga += wp[i] * wq[i];
-                }
-                if (ga == 0.0 || std::abs(ga) <= 1e-15 * std::sqrt(al * be)) continue;
-                rotated = true;
-                const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
-                for (idx i = 0; i < m; ++i) {
-                    const double x = wp[i], y = wq[i];
-                    wp[i] = c * x - sn * y;
-                    wq[i] = sn * x + c * y;
-                }
-                double* vp = Vw.col(p);
-                double* vq = Vw.col(q);
-                for (idx i = 0; i < n; ++i) {
-                    const double x = vp[i], y = vq[i];
-                    vp[i] = c * x - sn * y;
-                    vq[i] = sn * x + c * y;
-                }
+        int rotated = 0;
+        for (idx round = 0; round < np - 1; ++round) {
+#pragma omp parallel for schedule(static) reduction(| : rotated) if (par)
+            for (idx k = 0; k < np / 2; ++k) {
+                idx p = pos[static_cast<size_t>(k)], q = pos[static_cast<size_t>(np - 1 - k)];
+                if (p >= n || q >= n) continue;
+                if (p > q) std::swap(p, q);
+                if (jacobi_rotate(W.col(p), W.col(q), Vw.col(p), Vw.col(q), m, n)) rotated |= 1;
             }
+            // circle method: player 0 stays, the others rotate one place
+            const idx last = pos[static_cast<size_t>(np - 1)];
+            for (idx k = np - 1; k > 1; --k) pos[static_cast<size_t>(k)] = pos[static_cast<size_t>(k - 1)];
+            pos[1] = last;
+        }
         if (!rotated) break;
     }
     std::vector<double> sv(static_cast<size_t>(n));
