@@ -224,19 +224,19 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
     SLAB_T(0, 5);
     SLAB_T(0, 6);
+    // consecutive threads take consecutive doubles of a warp slice (8 x 8 fragment blocks,
+    // row-major inside: conflict-free shared loads); rows past dim and columns past K are padding
     double* outp = a.partial + (int64_t)blockIdx.x * a.dim * a.K;
-    for (int e = tid; e < dim * a.K; e += kTCons * 32) {
-        const int k = e / dim;
-        const int d = e - k * dim;
-        // row d lives in half h = d / (8 MTW), tile mt, fragment row q; column k in tile jn at
-        // lane 4 q + (k & 7) / 2, element k & 1
-        const int h = d / (8 * MTW), dm = d - 8 * MTW * h;
-        const int mt = dm >> 3, qq = dm & 7, jn = k >> 3, kk = k & 7;
-        const int off = ((mt * NT + jn) << 6) + 2 * (4 * qq + (kk >> 1)) + (kk & 1);
-        double sacc = 0.0;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) sacc += lds64(rbase + 8u * (uint32_t)((g + 4 * h) * slice + off));
-        outp[d + a.dim * k] = sacc;
+    constexpr int kBlk = MTW * NT;  // fragment blocks per warp slice
+    for (int e = tid; e < 2 * kBlk * 64; e += kTCons * 32) {
+        const int blk = e >> 6, w = e & 63;
+        const int h = blk / kBlk, rem = blk - h * kBlk;
+        const int mt = rem / NT, jn = rem - mt * NT;
+        const int d = 8 * (h * MTW + mt) + (w >> 3), k = 8 * jn + (w & 7);
+        if (d >= dim || k >= a.K) continue;
+        const uint32_t o = rbase + 8u * (uint32_t)(4 * h * slice + (rem << 6) + w);
+        const double v0 = lds64(o), v1 = lds64(o + 8u * slice), v2 = lds64(o + 16u * slice), v3 = lds64(o + 24u * slice);
+        outp[d + a.dim * k] = ((0.0 + v0) + v1 + v2) + v3;
     }
     SLAB_T(0, 4);
 }
