@@ -358,35 +358,38 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             SK_ADD(4, c3 - c2);
         }
     }
-    // fixed-order reduction over the 4 k-step groups through (consumed) stage 0;
-    // the two halves of a group write disjoint rows
+    // fixed-order sum over the 4 k-step groups: every consumer warp parks its accumulators in its
+    // own slice of the (consumed) stages in fragment order, then one pass adds the groups in order
+    // 0..3, consecutive threads reading consecutive doubles (conflict-free)
     SK_T(e0);
     if (threadIdx.x == 0) SK_ADD(7, e0 - k0);
     griddep_launch_dependents();
-    asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
-    double* red = stages;
-    const int ld = 8 * a.mtiles;
-    for (int g = 0; g < 4; ++g) {
-        if (tg == g) {
+    const uint32_t rbase = smem_u32(stages);
+    constexpr int kBlk = MTW * NT;  // 8 x 8 fragment blocks per warp slice
+    const int slice = kBlk * 64;
+    asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));  // every warp is done with the stages
+    {
+        const uint32_t mine = rbase + 8u * (uint32_t)(warp * slice);
 #pragma unroll
-            for (int mt = 0; mt < MTW; ++mt) {
-                if (mt < my_mt) {
+        for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
-                    for (int jn = 0; jn < NT; ++jn) {
-                        double* p0 = red + (8 * (mt0 + mt) + q) + ld * (8 * jn + 2 * r);
-                        *p0 = (g == 0 ? 0.0 : *p0) + acc[mt][jn][0];
-                        p0[ld] = (g == 0 ? 0.0 : p0[ld]) + acc[mt][jn][1];
-                    }
-                }
+            for (int jn = 0; jn < NT; ++jn) {
+                sts64(mine + 8u * (uint32_t)(((mt * NT + jn) << 6) + 2 * lane), acc[mt][jn][0]);
+                sts64(mine + 8u * (uint32_t)(((mt * NT + jn) << 6) + 2 * lane + 1), acc[mt][jn][1]);
             }
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
     }
+    asm volatile("bar.sync 1, %0;" ::"n"(kSkCons * 32));
     double* out = a.partial + (int64_t)blockIdx.x * dim * a.K;
-    for (int e = tid; e < dim * a.K; e += kSkCons * 32) {
-        const int k = e / (int)dim;
-        const int d = e - k * (int)dim;
-        out[d + dim * k] = red[d + ld * k];
+    for (int e = tid; e < kSkGrp * kBlk * 64; e += kSkCons * 32) {
+        const int blk = e >> 6, w = e & 63;
+        const int gr = blk / kBlk, rem = blk - gr * kBlk;
+        const int mt = rem / NT, jn = rem - mt * NT;
+        if (mt >= mt_base + (gr < mt_extra ? 1 : 0)) continue;  // tile past this group's share
+        const int d = 8 * (gr * mt_base + min(gr, mt_extra) + mt) + (w >> 3), k = 8 * jn + (w & 7);
+        if (d >= dim || k >= a.K) continue;
+        const uint32_t o = rbase + 8u * (uint32_t)(4 * gr * slice + (rem << 6) + w);
+        const double v0 = lds64(o), v1 = lds64(o + 8u * slice), v2 = lds64(o + 16u * slice), v3 = lds64(o + 24u * slice);
+        out[d + dim * k] = ((0.0 + v0) + v1 + v2) + v3;
     }
     SK_T(k3);
     if (threadIdx.x == 0) SK_ADD(6, k3 - k0);
@@ -866,7 +869,10 @@ bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
     // register budget: (row tiles per warp) x (8-column groups) accumulators
     const int mtw = sk_mtw(dim);
     if (nt_for(K) > 4 || (nt_for(K) == 4 && mtw > 4)) return false;
-    return sk_plan(dim, K).nstg >= 2;
+    const SkPlan pl = sk_plan(dim, K);
+    // the epilogue parks every consumer warp's accumulators in the consumed stages
+    const size_t slices = (size_t)kSkCons * sk_mtw(dim) * nt_for(K) * 64 * 8;
+    return pl.nstg >= 2 && slices <= (size_t)pl.nstg * ((size_t)pl.CT * dim + pl.pad) * 8;
 }
 
 void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
