@@ -113,17 +113,19 @@ __global__ void k_omega_units(int64_t left, int LC, int64_t nunits, int K, int N
 
 // ------------------------------------------------------------------ sketch
 // One unit's 4 k-steps over NMT row tiles: fragments of a k-step first, then its MMAs.
+// X element (d = 8 (mt0 + mt) + q, l = 4 t + rl) of the swizzled stage is at
+// xoff[t] + 128 mt (doubles), xoff[t] = 128 mt0 + 16 q + 2 ((2 t + rl / 2) ^ q) + (rl & 1): the
+// swizzle depends on the thread and t only, so every load is a shared load with an immediate offset.
 template <int NMT, int MTW, int NT>
-__device__ __forceinline__ void slab_consume(double (&acc)[MTW][NT][2], const double* X, const double* O, int mt0,
-                                             int q, int rl, int lane) {
+__device__ __forceinline__ void slab_consume(double (&acc)[MTW][NT][2], uint32_t xs, uint32_t os, const int (&xoff)[4],
+                                             int lane) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         double bv[NT], av[NMT];
 #pragma unroll
-        for (int jn = 0; jn < NT; ++jn) bv[jn] = O[((t * NT + jn) << 5) + lane];
-        const int l = 4 * t + rl;
+        for (int jn = 0; jn < NT; ++jn) bv[jn] = lds64(os + 8u * (uint32_t)(((t * NT + jn) << 5) + lane));
 #pragma unroll
-        for (int mt = 0; mt < NMT; ++mt) av[mt] = X[swz(8 * (mt0 + mt) + q, l)];
+        for (int mt = 0; mt < NMT; ++mt) av[mt] = lds64(xs + 8u * (uint32_t)(xoff[t] + 128 * mt));
 #pragma unroll
         for (int mt = 0; mt < NMT; ++mt)
 #pragma unroll
@@ -191,16 +193,19 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
 #pragma unroll
         for (int jn = 0; jn < NT; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
     SLAB_T(0, 2);
+    int xoff[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) xoff[t] = 128 * mt0 + 16 * q + 2 * ((2 * t + (rl >> 1)) ^ q) + (rl & 1);
+    const uint32_t sbase = smem_u32(base);
     for (int64_t j = pair; j < nl; j += 4) {
         const int s = (int)(j % kStg);
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
-        const double* X = reinterpret_cast<const double*>(base + s * sbytes);
-        const double* O = reinterpret_cast<const double*>(base + s * sbytes + xbytes);
+        const uint32_t xs = sbase + (uint32_t)(s * sbytes), os = xs + (uint32_t)xbytes;
         // half 1 of an odd row-tile count runs one tile fewer: compile-time counts, no predication
         if (MTW > 1 && my_mt == MTW - 1)
-            slab_consume<(MTW > 1 ? MTW - 1 : 1), MTW, NT>(acc, X, O, mt0, q, rl, lane);
+            slab_consume<(MTW > 1 ? MTW - 1 : 1), MTW, NT>(acc, xs, os, xoff, lane);
         else
-            slab_consume<MTW, MTW, NT>(acc, X, O, mt0, q, rl, lane);
+            slab_consume<MTW, MTW, NT>(acc, xs, os, xoff, lane);
         __syncwarp();
         mbar_arrive(&empty[s]);
     }
@@ -304,10 +309,20 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         }
     const int pair = warp & 3, mt = warp >> 2;  // pair takes units j = pair (mod 4); mt = 8-row tile of l
     SLAB_T(1, 2);
+    // X element (d = perm_d(t, rl), l = 8 mt + q): d & 7 = c_{t & 1} = 2 (t & 1) + 4 (rl & 1) + rl / 2,
+    // so its swizzled offset is 128 (t / 2) + xo[t & 1] doubles (shared loads, immediate offsets)
+    int xo[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int c = 2 * p + ((rl & 1) ? 4 : 0) + (rl >> 1);
+        const int l = 8 * mt + q;
+        xo[p] = 16 * c + 2 * ((l >> 1) ^ c) + (l & 1);
+    }
+    const uint32_t sbase = smem_u32(base);
     for (int64_t j = pair; j < nl; j += 4) {
         const int s = (int)(j % kStg);
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
-        const double* X = reinterpret_cast<const double*>(base + s * sbytes);
+        const uint32_t xs = sbase + (uint32_t)(s * sbytes);
         double acc[2][NT][2];  // [k-step parity][column tile][pair]
 #pragma unroll
         for (int p = 0; p < 2; ++p)
@@ -316,7 +331,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
 #pragma unroll
         for (int t = 0; t < TKM; ++t) {
             if (t < a.Tk) {
-                const double av = X[swz(perm_d(t, rl), 8 * mt + q)];
+                const double av = lds64(xs + 8u * (uint32_t)(128 * (t >> 1) + xo[t & 1]));
 #pragma unroll
                 for (int jn = 0; jn < NT; ++jn) dmma884(acc[t & 1][jn][0], acc[t & 1][jn][1], av, qb[t][jn]);
             }
