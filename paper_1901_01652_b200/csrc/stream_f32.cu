@@ -36,6 +36,12 @@ namespace trg {
 namespace {
 
 constexpr int kF32Cons = 8;
+#ifndef TRG_F32_GEN_SMALL
+#define TRG_F32_GEN_SMALL 16  // generator warps when TK <= 12 (dense test-matrix tiles, C5)
+#endif
+#ifndef TRG_F32_GEN_LARGE
+#define TRG_F32_GEN_LARGE 4
+#endif
 constexpr int kF32Stages = 4;
 constexpr int kF32OB = 2;
 
@@ -116,6 +122,53 @@ __global__ void __launch_bounds__((kF32Cons + GEN + 1) * 32, 1)
     if (warp >= kF32Cons) {
         // ---- generators: Omega(c, k) = draw D + col_off + c + rows_glob k, pairs shared
         const int gtid = tid - kF32Cons * 32;
+        constexpr int kMaxSl = 4;  // slots per generator thread on the fast path
+        const bool even = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) == 0 && (CT & 1) == 0 &&
+                          (CT / 2) * a.K <= kMaxSl * kF32Gen * 32;
+        if (even) {
+            // Every column run starts on an even draw: slot (jj, k) writes rows 2jj, 2jj + 1 of
+            // column k (k fastest across lanes, so the stores fill consecutive words), and from
+            // one tile of this CTA to the next its pair index advances by GC CT / 2, i.e. the
+            // SplitMix64 state by GC CT gamma: no per-tile index arithmetic in the loop.
+            const int nslots = (CT / 2) * a.K;
+            const uint64_t gam = 0x9E3779B97F4A7C15ull;
+            const uint64_t inc = (uint64_t)GC * (uint64_t)CT * gam;
+            int jjs[kMaxSl], ks[kMaxSl];
+            uint64_t st[kMaxSl];
+            int ns = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxSl; ++i) {
+                const int sl = gtid + i * kF32Gen * 32;
+                const bool on = sl < nslots;
+                jjs[i] = on ? sl / a.K : 0;
+                ks[i] = on ? sl - jjs[i] * a.K : 0;
+                const uint64_t p0 = ((a.D + (uint64_t)a.col_off + (uint64_t)cg * CT +
+                                      (uint64_t)a.rows_glob * (uint64_t)ks[i]) >> 1) + (uint64_t)jjs[i];
+                st[i] = a.seed + (2ull * p0 + 1ull) * gam;
+                ns += on ? 1 : 0;
+            }
+            const int64_t full_tiles = a.L / CT;
+            for (int64_t j = 0; j < nl; ++j) {
+                const int b = (int)(j % kF32OB);
+                mbar_wait(&empty_o[b], (uint32_t)((j / kF32OB) & 1) ^ 1u);
+                const int64_t t = cg + j * GC;
+                const int64_t ncol = t < full_tiles ? CT : a.L - t * CT;
+                float* O = om + b * om_floats;
+#pragma unroll
+                for (int i = 0; i < kMaxSl; ++i) {
+                    if (i < ns) {
+                        float z0, z1;
+                        gauss_pair_f32_state(st[i], z0, z1);
+                        const int c = 2 * jjs[i];
+                        O[c * a.Kp + ks[i]] = c < ncol ? z0 : 0.f;
+                        O[(c + 1) * a.Kp + ks[i]] = c + 1 < ncol ? z1 : 0.f;
+                    }
+                    st[i] += inc;
+                }
+                mbar_arrive(&full_o[b]);
+            }
+            return;
+        }
         const int npmax = CT / 2 + 1;
         for (int64_t j = 0; j < nl; ++j) {
             const int b = (int)(j % kF32OB);
@@ -452,7 +505,7 @@ int launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* partia
     cudaMemsetAsync(partial, 0, sizeof(double) * gc * sp.dim * sp.K, s);
 #define TRG_F32(TKV)                                                                                          \
     do {                                                                                                      \
-        constexpr int G = TKV <= 12 ? 8 : 4;                                                                  \
+        constexpr int G = TKV <= 12 ? TRG_F32_GEN_SMALL : TRG_F32_GEN_LARGE;                                  \
         cudaFuncSetAttribute(k_sketch_l1_f32<TKV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem); \
         k_sketch_l1_f32<TKV, G><<<grid, (kF32Cons + G + 1) * 32, p.smem, s>>>(map, a);                        \
     } while (0)
