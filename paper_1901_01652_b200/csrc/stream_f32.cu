@@ -289,7 +289,7 @@ constexpr int kTtStages = 8;  // two per consumer warp
 
 struct F32TtArgs {
     int64_t I0, L;  // X_(0) is I0 x L (fibres of I0)
-    int DC, NCH, K, Kp;
+    int DC, NCH, K, Kp;  // K outputs in all (row stride of out); CTA row blockIdx.y owns KP of them
     int64_t nunits;  // ceil(L / 64)
     double* out;     // P^(1) promoted to fp64: row m, K outputs (o fastest); later modes run fp64
 };
@@ -309,9 +309,10 @@ __global__ void __launch_bounds__((kTtCons + 1) * 32, 1)
     // units of this CTA: u = blockIdx.x + i * gridDim.x; warp w owns i = w, w + 4, ...
     const int64_t nu = (a.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t nrounds = (nu + kTtCons - 1) / kTtCons;  // unit rounds (each warp one unit per round)
+    const int ko = blockIdx.y * KP;  // first output column of this CTA's group
     for (int e = tid; e < qrows * KP; e += blockDim.x) {
         const int d = e / KP, o = e - d * KP;
-        Qs[e] = (d < a.I0 && o < a.K) ? (float)q[d + ldq * o] : 0.f;
+        Qs[e] = (d < a.I0 && ko + o < a.K) ? (float)q[d + ldq * (ko + o)] : 0.f;
     }
     if (tid == 0) {
         for (int s = 0; s < kTtStages; ++s) {
@@ -389,10 +390,10 @@ __global__ void __launch_bounds__((kTtCons + 1) * 32, 1)
         for (int f = 0; f < 2; ++f) {
             const int64_t m = u * 64 + lane + 32 * f;
             if (m >= a.L) continue;
-            double* dst = a.out + m * a.K;
+            double* dst = a.out + m * a.K + ko;
 #pragma unroll
             for (int o = 0; o < KP; ++o)
-                if (o < a.K) dst[o] = (double)acc[f][o];
+                if (ko + o < a.K) dst[o] = (double)acc[f][o];
         }
     }
 }
@@ -522,12 +523,16 @@ int launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* partia
     return gc;
 }
 
+// outputs per CTA: all of them up to 24; beyond (C4's K_0 = 64) groups of 16 on grid.y, whose CTAs
+// walk the same fibre units at the same time so the repeated X tiles come from L2
+int ttm_f32_kp(int64_t K) { return K <= 24 ? (int)((K + 3) & ~3) : 16; }
+
 bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols) {
-    if (dtype != F32 || left != 1 || (dim % 4) != 0 || K > 24 || ncols >= (int64_t(1) << 31) || !encode_fn())
+    if (dtype != F32 || left != 1 || (dim % 4) != 0 || K > 128 || ncols >= (int64_t(1) << 31) || !encode_fn())
         return false;
     const int DC = odd_quad(std::min<int>(60, (int)dim));
     const int NCH = (int)((dim + DC - 1) / DC);
-    const int Kp = (int)((K + 3) & ~3);
+    const int Kp = ttm_f32_kp(K);
     const size_t smem = (size_t)kTtStages * 64 * DC * 4 + (size_t)NCH * DC * Kp * 4 + 256;
     return smem <= 220 * 1024;
 }
@@ -540,7 +545,7 @@ void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const do
     a.DC = odd_quad(std::min<int>(60, (int)p.dim));
     a.NCH = (int)((p.dim + a.DC - 1) / a.DC);
     a.K = (int)p.odim;
-    a.Kp = (int)((p.odim + 3) & ~3);
+    a.Kp = ttm_f32_kp(p.odim);
     a.nunits = (p.right + 63) / 64;
     a.out = reinterpret_cast<double*>(out);
     CUtensorMap map;
@@ -552,7 +557,9 @@ void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const do
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const size_t smem = (size_t)kTtStages * 64 * a.DC * 4 + (size_t)a.NCH * a.DC * a.Kp * 4 + 256;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
+    const int groups = (int)((a.K + a.Kp - 1) / a.Kp);
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, std::max(1, num_sms / groups)));
+    const dim3 grid(gx, groups);
     const int threads = (kTtCons + 1) * 32;
 #define TRG_TT(KPV)                                                                                     \
     do {                                                                                                \
