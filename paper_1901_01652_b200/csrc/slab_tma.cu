@@ -49,7 +49,15 @@ __device__ long long g_slab_prof[2][8];
 #define SLAB_T(kind, i)
 #endif
 
-constexpr int kTCons = 8;    // consumer warps: pairs (w, w + 4) share a unit, two per SM sub-partition
+constexpr int kTCons = 8;    // shrink consumer warps: pairs (w, w + 4) share a unit, two per SM sub-partition
+#ifndef TRG_SLAB_SCONS
+#define TRG_SLAB_SCONS 8  // 12 measured the same on C2 (profiles/README.md)
+#endif
+// sketch consumer warps: teams (w & 3) of kSGrp warps share a unit, one team per SM sub-partition,
+// team member w >> 2 taking one of kSGrp balanced groups of the 8-row tiles
+constexpr int kSCons = TRG_SLAB_SCONS;
+constexpr int kSGrp = kSCons / 4;
+static_assert(kSCons % 4 == 0 && kSGrp >= 1 && kSGrp <= 4, "slab sketch consumers: 4, 8, 12 or 16 warps");
 constexpr int kMaxStg = 8;  // stages (units in flight): 8 measured best (16 was slower on C2/C5 mode 1)
 constexpr int kUnitL = 16;   // left-chunk width of a unit (16 doubles = 128 B rows)
 
@@ -134,7 +142,7 @@ __device__ __forceinline__ void slab_consume(double (&acc)[MTW][NT][2], uint32_t
 }
 
 template <int MTW, int NT>
-__global__ void __launch_bounds__((kTCons + 1) * 32, 1)
+__global__ void __launch_bounds__((kSCons + 1) * 32, 1)
     k_slab2_sketch_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SLAB_T(0, 0);
@@ -161,12 +169,12 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     if (tid == 0) {
         for (int s = 0; s < kStg; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 64);
+            mbar_init(&empty[s], kSGrp * 32);
         }
         fence_mbar_init();
     }
     __syncthreads();
-    if (warp == kTCons) {
+    if (warp == kSCons) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             for (int64_t j = 0; j < nl; ++j) {
@@ -184,9 +192,10 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         return;
     }
     const int q = lane >> 2, rl = lane & 3;
-    const int pair = warp & 3, half = warp >> 2;  // pair takes units j = pair (mod 4); half takes 8-row tiles
-    const int mt0 = half * MTW;
-    const int my_mt = min(MTW, a.mtiles - mt0);
+    const int pair = warp & 3, grp = warp >> 2;  // team `pair` takes units j = pair (mod 4)
+    const int mt_base = a.mtiles / kSGrp, mt_extra = a.mtiles % kSGrp;
+    const int mt0 = grp * mt_base + min(grp, mt_extra);
+    const int my_mt = mt_base + (grp < mt_extra ? 1 : 0);
     double acc[MTW][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MTW; ++mt)
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         const int s = (int)(j % kStg);
         mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
         const uint32_t xs = sbase + (uint32_t)(s * sbytes), os = xs + (uint32_t)xbytes;
-        // half 1 of an odd row-tile count runs one tile fewer: compile-time counts, no predication
+        // groups past mt_extra run one tile fewer: compile-time counts, no predication
         if (MTW > 1 && my_mt == MTW - 1)
             slab_consume<(MTW > 1 ? MTW - 1 : 1), MTW, NT>(acc, xs, os, xoff, lane);
         else
@@ -209,13 +218,13 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         __syncwarp();
         mbar_arrive(&empty[s]);
     }
-    // fixed-order sum of the four pairs' partials: every consumer warp parks its accumulators in
-    // its own slice of the (consumed) stages, then one pass adds the pairs in order 0..3
+    // fixed-order sum of the four teams' partials: every consumer warp parks its accumulators in
+    // its own slice of the (consumed) stages, then one pass adds the teams in order 0..3
     SLAB_T(0, 3);
     griddep_launch_dependents();
     const uint32_t rbase = smem_u32(base);
     const int slice = MTW * NT * 64;  // doubles per warp
-    asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));  // every warp is done with the stages
+    asm volatile("bar.sync 1, %0;" ::"n"(kSCons * 32));  // every warp is done with the stages
     {
         const uint32_t mine = rbase + 8u * (uint32_t)(warp * slice);
 #pragma unroll
@@ -226,18 +235,19 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
                 sts64(mine + 8u * (uint32_t)(((mt * NT + jn) << 6) + 2 * lane + 1), acc[mt][jn][1]);
             }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kTCons * 32));
+    asm volatile("bar.sync 1, %0;" ::"n"(kSCons * 32));
     SLAB_T(0, 5);
     SLAB_T(0, 6);
     // consecutive threads take consecutive doubles of a warp slice (8 x 8 fragment blocks,
     // row-major inside: conflict-free shared loads); rows past dim and columns past K are padding
     double* outp = a.partial + (int64_t)blockIdx.x * a.dim * a.K;
     constexpr int kBlk = MTW * NT;  // fragment blocks per warp slice
-    for (int e = tid; e < 2 * kBlk * 64; e += kTCons * 32) {
+    for (int e = tid; e < kSGrp * kBlk * 64; e += kSCons * 32) {
         const int blk = e >> 6, w = e & 63;
         const int h = blk / kBlk, rem = blk - h * kBlk;
         const int mt = rem / NT, jn = rem - mt * NT;
-        const int d = 8 * (h * MTW + mt) + (w >> 3), k = 8 * jn + (w & 7);
+        if (mt >= mt_base + (h < mt_extra ? 1 : 0)) continue;  // tile past this group's share
+        const int d = 8 * (h * mt_base + min(h, mt_extra) + mt) + (w >> 3), k = 8 * jn + (w & 7);
         if (d >= dim || k >= a.K) continue;
         const uint32_t o = rbase + 8u * (uint32_t)(4 * h * slice + (rem << 6) + w);
         const double v0 = lds64(o), v1 = lds64(o + 8u * slice), v2 = lds64(o + 16u * slice), v3 = lds64(o + 24u * slice);
@@ -469,14 +479,14 @@ int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_
     a.S = stages_for(sketch_stage(p.dim, NT));
     const size_t smem = slab_smem(sketch_stage(p.dim, NT), a.S);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
-    const int threads = (kTCons + 1) * 32;
+    const int threads = (kSCons + 1) * 32;
 #define TRG_S2(MTW, NTV)                                                  \
     do {                                                                  \
         set_smem(k_slab2_sketch_f64<MTW, NTV>, smem);                     \
         pdl_launch(k_slab2_sketch_f64<MTW, NTV>, dim3(grid), dim3(threads), smem, s, map, a); \
     } while (0)
-    // row tiles per half: ceil(mtiles / 2), exact (half 1 takes the remainder)
-    switch ((a.mtiles + 1) / 2) {
+    // row tiles per group: ceil(mtiles / kSGrp) (the later groups take one fewer when uneven)
+    switch ((a.mtiles + kSGrp - 1) / kSGrp) {
 #define TRG_S2_NT(M) if (NT == 1) TRG_S2(M, 1); else TRG_S2(M, 2); break;
         case 1: TRG_S2_NT(1)
         case 2: TRG_S2_NT(2)
