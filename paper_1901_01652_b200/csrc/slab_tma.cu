@@ -137,7 +137,13 @@ __device__ __forceinline__ void slab_consume(double (&acc)[MTW][NT][2], uint32_t
 #pragma unroll
         for (int mt = 0; mt < NMT; ++mt)
 #pragma unroll
-            for (int jn = 0; jn < NT; ++jn) dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
+            for (int jn = 0; jn < NT; ++jn) {
+#ifdef TRG_DBG_NO_MMA  // development: tensor work removed (timing only)
+                acc[mt][jn][0] += av[mt] * bv[jn];
+#else
+                dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
+#endif
+            }
     }
 }
 
@@ -184,9 +190,14 @@ __global__ void __launch_bounds__((kSCons + 1) * 32, 1)
                 const int64_t r = u / a.LC;
                 const int lc = (int)(u - r * a.LC);
                 unsigned char* st = base + s * sbytes;
+#ifdef TRG_DBG_NO_OMEGA_LOAD  // development: the test-matrix blocks not loaded (timing only)
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128));
+                tma_load_2d(st, &tmap, kUnitL * lc, (int)(a.dim * r), &full[s], pol);
+#else
                 mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128 + obytes));
                 tma_load_2d(st, &tmap, kUnitL * lc, (int)(a.dim * r), &full[s], pol);
                 bulk_g2s(st + xbytes, a.omega + u * (int64_t)(4 * NT * 32), (uint32_t)obytes, &full[s], pol);
+#endif
             }
         }
         return;
