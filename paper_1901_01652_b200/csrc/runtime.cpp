@@ -379,7 +379,9 @@ std::vector<ModeOffsets> sketch_offsets(const std::vector<int64_t>& dims, const 
 struct PreOmega {
     double* buf = nullptr;
     cudaEvent_t ready = nullptr;
-    bool joined = false;  // main stream already waits on `ready`
+    bool joined = false;   // main stream already waits on `ready`
+    bool pending = false;  // `buf` not generated yet: a QR launch on the main stream takes `job`
+    trg::OmegaUnitsJob job;
 };
 
 // Per-CTA partial sums of Y_n left for the QR launch to reduce (launch_qr_fused)
@@ -427,15 +429,15 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     } else if (p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
         const int NT = Kn <= 8 ? 1 : 2;
         double* om = nullptr;
-        if (pre && pre->buf) {
-            om = pre->buf;
-            if (pre->ready && !pre->joined) CK(cudaStreamWaitEvent(ctx->stream, pre->ready, 0));
-        } else {
-            om = (double*)ctx->tmp(sizeof(double) * trg::slab2_units(p.left, p.right) * 4 * NT * 32);
+        const bool have = pre && pre->buf;
+        om = have ? pre->buf : (double*)ctx->tmp(sizeof(double) * trg::slab2_units(p.left, p.right) * 4 * NT * 32);
+        if (have && pre->ready && !pre->joined) CK(cudaStreamWaitEvent(ctx->stream, pre->ready, 0));
+        if (!have || pre->pending) {  // no earlier launch generated the blocks: do it here
             ctx->launch("omega_m" + std::to_string(n), [&] {
                 trg::launch_omega_units(p.left, p.right, (int)Kn, p.seed, p.D, p.col_off, p.rows_glob, om,
                                         ctx->stream);
-            }, 2);
+            });
+            if (have) pre->pending = false;
         }
         partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
         int grid = 0;
@@ -508,8 +510,11 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
     return out;
 }
 
+// in_launch: only allocate the blocks and record the jobs; the main stream's QR launches generate
+// them on their idle CTAs (launch_qr_fused), or the sketch of that mode does if none could
 void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const std::vector<int64_t>& K, uint64_t seed,
-                        const std::vector<ModeOffsets>& offs, int after, std::vector<PreOmega>& pre) {
+                        const std::vector<ModeOffsets>& offs, int after, std::vector<PreOmega>& pre,
+                        bool in_launch = false) {
     const int N = (int)x->dims.size();
     std::vector<int64_t> shape = x->local_shape();
     for (int m = 0; m <= after; ++m) shape[m] = K[m];
@@ -522,12 +527,19 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const s
         if (left > 1 && trg::slab2_ok(later_dt, left, dim, K[m], right)) {
             const int NT = K[m] <= 8 ? 1 : 2;
             pre[m].buf = (double*)ctx->tmp(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
+            if (in_launch) {
+                pre[m].job = trg::omega_units_job(left, right, (int)K[m], seed, offs[m].D, offs[m].col_off,
+                                                  offs[m].rows_glob, pre[m].buf);
+                pre[m].pending = true;
+                shape[m] = K[m];
+                continue;
+            }
             CK(cudaEventRecord(go, ctx->stream));
             CK(cudaStreamWaitEvent(ctx->side, go, 0));
             trg::launch_omega_units(left, right, (int)K[m], seed, offs[m].D, offs[m].col_off, offs[m].rows_glob,
                                     pre[m].buf, ctx->side);
             CK(cudaGetLastError());
-            ctx->launches += 2;
+            ctx->launches += 1;
             CK(cudaEventCreateWithFlags(&pre[m].ready, cudaEventDisableTiming));
             CK(cudaEventRecord(pre[m].ready, ctx->side));
         }
@@ -738,13 +750,21 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     };
 
     std::vector<YParts> yparts(N);
+    std::vector<PreOmega> pre(N);
     auto qr = [&](int n) {
         const int64_t In = x->dims[n], Kn = sk->K[n];
         double* work = (double*)ctx->tmp(sizeof(double) * In * Kn);
         if (yparts[n].partial) {
+            // the launch's CTAs past the reduce generate the next pending test matrix
+            const trg::OmegaUnitsJob* job = nullptr;
+            for (int m = n + 1; m < N && !job && yparts[n].nparts > 1; ++m)  // runs iff ticketed
+                if (pre[m].pending) {
+                    job = &pre[m].job;
+                    pre[m].pending = false;
+                }
             ctx->launch("qr", [&] {
                 trg::launch_qr_fused(yparts[n].partial, yparts[n].nparts, In, (int)Kn, sk->dY[n], sk->dQ[n], work,
-                                     sk->dflags + n, sk->dflags + 2 * N + n, ctx->stream);
+                                     sk->dflags + n, sk->dflags + 2 * N + n, ctx->stream, job, ctx->num_sms);
             });
             ctx->tmp_free(yparts[n].partial);
             yparts[n] = YParts{};
@@ -754,7 +774,6 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         ctx->tmp_free(work);
     };
 
-    std::vector<PreOmega> pre(N);
     bool pre_started = false;
     if (variant == TRG_SEQUENTIAL) {
         std::vector<bool> y_ready(N, false);
@@ -762,6 +781,15 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
             if (!y_ready[n]) sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n]);
+            static const bool side_omega = getenv("TRG_SIDE_OMEGA") != nullptr;
+            if (!pre_started && yparts[n].partial && !side_omega) {
+                // ticketed QR launches: their CTAs past the reduce generate the later test
+                // matrices (one mode per launch), in the latency-bound QR instead of next to the
+                // HBM-bound shrink
+                pre_started = true;
+                const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
+                schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre, true);
+            }
             qr(n);
             if (!pre_started) {
                 // Omega_m of every later slab-kernel mode depends only on shapes and the seed:

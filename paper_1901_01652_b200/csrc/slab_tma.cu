@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "launch.h"
+#include "omega_units.cuh"
 #include "pipeline.cuh"
 
 namespace trg {
@@ -60,6 +61,7 @@ constexpr int kSGrp = kSCons / 4;
 static_assert(kSCons % 4 == 0 && kSGrp >= 1 && kSGrp <= 4, "slab sketch consumers: 4, 8, 12 or 16 warps");
 constexpr int kMaxStg = 8;  // stages (units in flight): 8 measured best (16 was slower on C2/C5 mode 1)
 constexpr int kUnitL = 16;   // left-chunk width of a unit (16 doubles = 128 B rows)
+static_assert(kUnitL == kOmegaUnitL, "unit width shared with omega_units.cuh");
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
                                             uint64_t pol) {
@@ -86,37 +88,12 @@ struct Slab2Args {
 };
 
 // ------------------------------------------------------------------ test-matrix unit blocks
-// block u, element (t, jn, lane) = Omega(c, k), c = 16 lc + 4 t + (lane & 3) (zero past
-// `left`), k = 8 jn + (lane >> 2) (zero past K); Omega(c, k) = reference draw
-// D + col_off + c + left r + rows_glob k (sketch.hpp:32-38).
-// One CTA iteration per unit, one thread per (k, pair) slot of it: no 64-bit
-// division in the per-draw path (the unit -> (r, lc) split is once per unit).
-__global__ void k_omega_units(int64_t left, int LC, int64_t nunits, int K, int NT, uint64_t seed, uint64_t D,
-                              int64_t col_off, int64_t rows_glob, const GaussTables* gt, double* out) {
+// (omega_units.cuh)
+__global__ void k_omega_units(OmegaUnitsJob j) {
     __shared__ GaussTables tabs;
-    gauss_tables_to_smem(tabs, gt);
+    gauss_tables_to_smem(tabs, j.gt);
     __syncthreads();
-    constexpr int npp = kUnitL / 2 + 1;  // pairs covering 16 consecutive draws
-    const int slot = threadIdx.x;
-    const int k = slot / npp, jj = slot - k * npp;
-    if (k >= K) return;
-    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int64_t r = LC == 1 ? u : u / LC;
-        const int lc = (int)(u - r * LC);
-        const uint64_t s0 = D + (uint64_t)(col_off + kUnitL * lc + left * r) + (uint64_t)rows_glob * (uint64_t)k;
-        const uint64_t p = (s0 >> 1) + (uint64_t)jj;
-        if (p > ((s0 + kUnitL - 1) >> 1)) continue;
-        double z[2];
-        gauss_pair_tab(seed, p, tabs, z[0], z[1]);
-        double* blk = out + u * (int64_t)(4 * NT * 32);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int l = (int)(2ull * p - s0) + e;  // 0..15 within the unit
-            if (l < 0 || l >= kUnitL) continue;
-            const bool live = kUnitL * lc + l < left;
-            blk[(((l >> 2) * NT + (k >> 3)) << 5) + (l & 3) + ((k & 7) << 2)] = live ? z[e] : 0.0;
-        }
-    }
+    omega_units_cta(j, tabs, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------ sketch
@@ -451,16 +428,29 @@ bool slab2_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right) {
 
 int64_t slab2_units(int64_t left, int64_t right) { return right * ((left + kUnitL - 1) / kUnitL); }
 
+OmegaUnitsJob omega_units_job(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
+                              int64_t rows_glob, double* out) {
+    OmegaUnitsJob j;
+    j.out = out;
+    j.left = left;
+    j.LC = (int)((left + kUnitL - 1) / kUnitL);
+    j.nunits = right * j.LC;
+    j.K = K;
+    j.NT = K <= 8 ? 1 : 2;
+    j.seed = seed;
+    j.D = D;
+    j.col_off = col_off;
+    j.rows_glob = rows_glob;
+    return j;
+}
+
 void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
                         int64_t rows_glob, double* out, cudaStream_t s) {
-    const int LC = (int)((left + kUnitL - 1) / kUnitL);
-    const int64_t nunits = right * LC;
-    const int NT = K <= 8 ? 1 : 2;
-    cudaMemsetAsync(out, 0, sizeof(double) * nunits * 4 * NT * 32, s);
-    const int threads = ((K * (kUnitL / 2 + 1)) + 31) & ~31;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, 148 * 12));
-    k_omega_units<<<blocks, threads, 0, s>>>(left, LC, nunits, K, NT, seed, D, col_off, rows_glob, gauss_tables(s),
-                                             out);
+    OmegaUnitsJob j = omega_units_job(left, right, K, seed, D, col_off, rows_glob, out);
+    j.gt = gauss_tables(s);
+    const int threads = (omega_unit_slots(j.NT) + 31) & ~31;  // one unit per iteration, zeros included
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(j.nunits, 148 * 12));
+    k_omega_units<<<blocks, threads, 0, s>>>(j);
 }
 
 void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s) {

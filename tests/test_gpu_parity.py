@@ -292,4 +292,5 @@ def test_launch_counter_and_profiling(trg, ctx):
     labels = ctx.kernel_labels()
     assert "sketch_m0" in labels and "qr" in labels
     assert "ttm_m0" in labels or "ttm_m0+sketch_m1" in labels  # fused shrink + next sketch (K3)
-    assert ctx.launch_count() >= 10  # 3 modes x (sketch + reduce + qr + ttm), minus fused launches
+    # 3 modes x (sketch + qr + ttm); the later modes' test matrices come from the QR launches
+    assert ctx.launch_count() >= 9
