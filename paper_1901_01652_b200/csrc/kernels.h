@@ -43,6 +43,11 @@ struct TTMPlan {
     int64_t rows, nrowtiles;
     int grid_x;
     size_t smem;
+    // shrink of the projection chain (run_sketch): its input was completed two or more grids back,
+    // so the register-Q kernels prefetch it before the grid dependency on the QR resolves, and
+    // they leave `spare_sms` SMs to the QR launch they follow
+    bool chain = false;
+    int spare_sms = 0;
 };
 void plan_ttm(TTMPlan& p, int num_sms);
 void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cudaStream_t s);

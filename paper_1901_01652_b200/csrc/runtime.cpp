@@ -471,9 +471,13 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
 // out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
 // out = cur x_n Q^T; *odt is the output dtype (fp32 mode-0 input is promoted to fp64 by its shrink)
 void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
-                  int n, int64_t Kn, const double* dQ, int* odt, bool escape = true) {
+                  int n, int64_t Kn, const double* dQ, int* odt, bool escape = true, bool chain = false) {
     const int N = (int)cur_shape.size();
     trg::TTMPlan p{};
+    static const int spare = getenv("TRG_TTM_SPARE") ? atoi(getenv("TRG_TTM_SPARE")) : 0;
+    static const bool late = getenv("TRG_QR_LATE") != nullptr;
+    p.chain = chain && !late;
+    p.spare_sms = spare;
     p.dtype = cdt;
     p.left = prod(cur_shape, 0, n);
     p.dim = cur_shape[n];
@@ -834,7 +838,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 owned_arena = true;
             } else {
                 int odt = cdt;
-                out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt, escape);
+                out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt, escape, /*chain=*/true);
                 cdt = odt;
                 release_owned();
                 owned = out;

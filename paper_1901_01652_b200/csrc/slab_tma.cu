@@ -85,6 +85,7 @@ struct Slab2Args {
     double* out;               // ttm
     const double* q;           // ttm: Q (ldq x K col-major)
     int64_t ldq;
+    int chain;                 // ttm: TTMPlan::chain, only the consumers wait on the grid dependency
 };
 
 // ------------------------------------------------------------------ test-matrix unit blocks
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     k_slab2_ttm_f64(const __grid_constant__ CUtensorMap tmap, Slab2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SLAB_T(1, 0);
-    griddep_wait();
+    if (!a.chain) griddep_wait();
     SLAB_T(1, 1);
     const int dim = (int)a.dim;
     const int rows_pad = (dim + 7) & ~7;
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     }
     // B fragments of Q in registers: qb[t][jn] = Q(d = perm_d(t, rl), o = 8 jn + q), loaded while
     // the producer's first tiles are in flight
+    if (a.chain) griddep_wait();  // Q is the preceding QR launch's output
     double qb[TKM][NT];
 #pragma unroll
     for (int t = 0; t < TKM; ++t)
@@ -529,8 +531,9 @@ void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double*
     a.ldq = ldq;
     const int NT = a.K <= 8 ? 1 : 2;
     a.S = stages_for(ttm_stage(p.dim));
+    a.chain = p.chain ? 1 : 0;
     const size_t smem = slab_smem(ttm_stage(p.dim), a.S);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nunits, num_sms - (p.chain ? p.spare_sms : 0)));
     const int threads = (kTCons + 1) * 32;
 #define TRG_T2(NTV, TKV)                                                  \
     do {                                                                  \

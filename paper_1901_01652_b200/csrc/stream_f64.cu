@@ -401,6 +401,7 @@ struct TtmArgs {
     const double* q;  // Q (ldq x K column-major): out(m, o) = sum_d x(m, d) Q(d, o)
     int64_t dim, rows, ntiles, ldq;
     int K, MT, Tk;
+    int chain;  // TTMPlan::chain: only the consumers wait on the grid dependency (they read Q)
 };
 
 template <int NT>
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__((kFCons + kFGen + 1) * 32, 1) k_ttm_sketch_l1_
 template <int MTO, int TKM>
 __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    griddep_wait();
+    if (!a.chain) griddep_wait();
     const int64_t dim = a.dim;
     const int MT = a.MT;
     const int stage_elems = (int)(MT * dim) + kPad;
@@ -762,6 +763,7 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
     }
     // A fragments of Q^T, loaded while the producer's first tiles are in flight:
     // qa[mt][t] = Q^T(o = 8 mt + q, d = 4 t + r) = Q(d, o)
+    if (a.chain) griddep_wait();  // Q is the preceding QR launch's output
     double qa[MTO][TKM];
 #pragma unroll
     for (int mt = 0; mt < MTO; ++mt)
@@ -959,10 +961,13 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
     a.MT = 16 * kCons;
     a.Tk = (int)((p.dim + 3) / 4);
     a.ntiles = (a.rows + a.MT - 1) / a.MT;
+    a.chain = 0;
     const int NT = nt_for(a.K);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     const int threads = (kCons + 1) * 32;
     if (a.K <= 16 && a.Tk <= 32) {  // Q^T resident in registers
+        a.chain = p.chain ? 1 : 0;
+        if (p.chain) grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms - p.spare_sms));
         const size_t smem = kStages * (size_t)(a.MT * a.dim + kPad) * 8 + kBarBytes;
 #define TRG_QR(MTO, TKM)                                                  \
     do {                                                                  \
