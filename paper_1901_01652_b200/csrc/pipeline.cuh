@@ -55,6 +55,18 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return pol;
 }
 
+// kind 0: evict_first, 1: evict_normal, 2: evict_last (a later kernel of the chain re-reads the data)
+__device__ __forceinline__ uint64_t policy_l2(int kind) {
+    uint64_t pol;
+    if (kind == 2)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else if (kind == 1)
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 // Global -> shared bulk copy (TMA, non-tensor). dst/src 16-B aligned, bytes % 16 == 0.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(

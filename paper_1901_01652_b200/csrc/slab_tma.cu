@@ -86,6 +86,8 @@ struct Slab2Args {
     const double* q;           // ttm: Q (ldq x K col-major)
     int64_t ldq;
     int chain;                 // ttm: TTMPlan::chain, only the consumers wait on the grid dependency
+    int rev;                   // units in descending order
+    int pol;                   // L2 policy of the X reads (policy_l2)
 };
 
 // ------------------------------------------------------------------ test-matrix unit blocks
@@ -160,11 +162,12 @@ __global__ void __launch_bounds__((kSCons + 1) * 32, 1)
     __syncthreads();
     if (warp == kSCons) {
         if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
+            const uint64_t pol = policy_l2(a.pol);
             for (int64_t j = 0; j < nl; ++j) {
                 const int s = (int)(j % kStg);
                 mbar_wait(&empty[s], (uint32_t)((j / kStg) & 1) ^ 1u);
-                const int64_t u = blockIdx.x + j * gridDim.x;
+                const int64_t u0 = blockIdx.x + j * gridDim.x;
+                const int64_t u = a.rev ? a.nunits - 1 - u0 : u0;
                 const int64_t r = u / a.LC;
                 const int lc = (int)(u - r * a.LC);
                 unsigned char* st = base + s * sbytes;
@@ -282,11 +285,12 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     __syncthreads();
     if (warp == kTCons) {
         if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
+            const uint64_t pol = policy_l2(a.pol);
             for (int64_t j = 0; j < nl; ++j) {
                 const int s = (int)(j % kStg);
                 mbar_wait(&empty[s], (uint32_t)((j / kStg) & 1) ^ 1u);
-                const int64_t u = blockIdx.x + j * gridDim.x;
+                const int64_t u0 = blockIdx.x + j * gridDim.x;
+                const int64_t u = a.rev ? a.nunits - 1 - u0 : u0;
                 const int64_t r = u / a.LC;
                 const int lc = (int)(u - r * a.LC);
                 mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128));
@@ -338,7 +342,8 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         }
         __syncwarp();
         mbar_arrive(&empty[s]);
-        const int64_t u = blockIdx.x + j * gridDim.x;
+        const int64_t u0 = blockIdx.x + j * gridDim.x;
+        const int64_t u = a.rev ? a.nunits - 1 - u0 : u0;
         const int64_t r = u / a.LC;
         const int lc = (int)(u - r * a.LC);
         // D fragment: (l = 8 mt + q, o = 8 jn + 2 rl + e) -> out(l_glob, o, r) at l + left (o + K r)
@@ -469,6 +474,12 @@ int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_
     CUtensorMap map;
     make_map(&map, x, p.left, p.dim * p.right, p.dim);
     Slab2Args a{};
+    // sweep switches (profiles/README.md): evict_first forward reads measured best here; the
+    // default priority lets this kernel's own misses evict the L2-resident tail of its input
+    static const int pol_env = getenv("TRG_POL_SLAB_SK") ? atoi(getenv("TRG_POL_SLAB_SK")) : 0;
+    static const int rev_env = getenv("TRG_REV_SLAB_SK") ? atoi(getenv("TRG_REV_SLAB_SK")) : 0;
+    a.pol = pol_env;
+    a.rev = rev_env;
     a.left = p.left;
     a.dim = p.dim;
     a.right = p.right;
@@ -519,6 +530,10 @@ void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double*
     CUtensorMap map;
     make_map(&map, in, p.left, p.dim * p.right, p.dim);
     Slab2Args a{};
+    static const int pol_env = getenv("TRG_POL_SLAB_TTM") ? atoi(getenv("TRG_POL_SLAB_TTM")) : 0;  // sweeps
+    static const int rev_env = getenv("TRG_REV_SLAB_TTM") ? atoi(getenv("TRG_REV_SLAB_TTM")) : 0;
+    a.pol = pol_env;
+    a.rev = rev_env;
     a.left = p.left;
     a.dim = p.dim;
     a.right = p.right;

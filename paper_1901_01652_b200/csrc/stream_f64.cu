@@ -62,6 +62,7 @@ struct SkArgs {
     uint64_t seed, D;
     double* partial;
     const GaussTables* gt;
+    int pol;  // L2 policy of the X reads (policy_l2)
 };
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     if (warp == kSkCons + kRng) {
         // ---------------- producer: TMA bulk copies of CT whole columns
         if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
+            const uint64_t pol = policy_l2(a.pol);
             for (int j = 0, s = 0, ph = 0; j < nl; ++j) {
                 mbar_wait(&empty_x[s], ph ^ 1);
                 const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
@@ -402,6 +403,7 @@ struct TtmArgs {
     int64_t dim, rows, ntiles, ldq;
     int K, MT, Tk;
     int chain;  // TTMPlan::chain: only the consumers wait on the grid dependency (they read Q)
+    int rev;    // tiles in descending order: the rows the chain's sketch read last are still in L2
 };
 
 template <int NT>
@@ -751,7 +753,8 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
             for (int j = 0; j < nl; ++j) {
                 const int s = j % kStages;
                 mbar_wait(&empty_x[s], ((j / kStages) & 1) ^ 1);
-                const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
+                const int64_t t0 = blockIdx.x + (int64_t)j * gridDim.x;
+                const int64_t t = a.rev ? a.ntiles - 1 - t0 : t0;
                 const int64_t m0 = t * MT;
                 const int64_t nrow = imin64(MT, a.rows - m0);
                 const uint32_t bytes = (uint32_t)(nrow * dim * 8);
@@ -795,7 +798,8 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_qreg_f64(TtmArgs a)
         }
         mbar_arrive(&empty_x[s]);
         // D fragment: out^T(o = 8 mt + q, row = 16 w + 8 nt + 2 r + e)
-        const int64_t m0 = (blockIdx.x + (int64_t)j * gridDim.x) * MT + 16 * warp;
+        const int64_t t0 = blockIdx.x + (int64_t)j * gridDim.x;
+        const int64_t m0 = (a.rev ? a.ntiles - 1 - t0 : t0) * MT + 16 * warp;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
@@ -880,6 +884,10 @@ bool stream_sketch_ok(int dtype, int64_t left, int64_t dim, int K) {
 void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
                           int* grid_out, cudaStream_t s) {
     SkArgs a;
+    // X with the default L2 priority, not evict_first: the shrink that follows re-reads X newest
+    // tile first (TtmArgs::rev) and finds the tail of it in L2 (ttm_m0 154 -> 146 us on C2)
+    static const int pol_env = (getenv("TRG_POL_SK0") ? atoi(getenv("TRG_POL_SK0")) : 1);
+    a.pol = pol_env;
     a.x = reinterpret_cast<const double*>(x);
     a.dim = p.dim;
     a.ncols = p.left * p.right;
@@ -962,6 +970,8 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
     a.Tk = (int)((p.dim + 3) / 4);
     a.ntiles = (a.rows + a.MT - 1) / a.MT;
     a.chain = 0;
+    static const bool fwd_env = getenv("TRG_TTM_FORWARD") != nullptr;  // development switch
+    a.rev = p.chain && !fwd_env ? 1 : 0;
     const int NT = nt_for(a.K);
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     const int threads = (kCons + 1) * 32;
