@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="sequential", choices=["sequential", "fused"])
+    ap.add_argument("--omega", default="gaussian", choices=["gaussian", "khatri_rao"],
+                    help="test matrices: the reference's Gaussian draws, or the opt-in Khatri-Rao products (f4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--decompose", type=int, default=1, help="also time the full trg_decompose_host once")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -308,6 +310,8 @@ def main():
     else:
         ctx = trg.Context(local)
     variant = L.TRG_FUSED if args.variant == "fused" else L.TRG_SEQUENTIAL
+    if args.omega == "khatri_rao":
+        variant |= L.TRG_OMEGA_KHATRI_RAO
 
     x, cores = make_tensor(ctx, cfg, seed=0)
     spec = trg.ProjectionSpec(cfg["K"], 0)
@@ -470,7 +474,7 @@ def main():
                 "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (reference random_factors + "
                 "noise at exact SNR, generated on device)",
                 "config": {"workload": workload_name(args.config, cfg), "dims": cfg["dims"], "K": cfg["K"],
-                           "variant": args.variant, "parallelism": f"last-mode shards x{world}" if world > 1
+                           "variant": args.variant, "omega": args.omega, "parallelism": f"last-mode shards x{world}" if world > 1
                            else "single GPU", "l2": "X larger than L2 (no flush needed)"},
                 "roofline": roof, "stage_roofline": stage, "cpu_baseline": cpu, "e2e": e2e, "decompose_e2e": decomp,
                 "gpu_launches": launches, "clocks": clk.summary(), "kernels": kernels}

@@ -53,7 +53,14 @@ enum trg_status {
 enum trg_dtype { TRG_F32 = 0, TRG_F64 = 1 };
 enum trg_variant {
     TRG_SEQUENTIAL = 0, /* reference sketch(): sequential shrinking, sketch.hpp:62-89 */
-    TRG_FUSED = 1       /* SPEC.md:319 alternative: every Y_n from the original X */
+    TRG_FUSED = 1,      /* SPEC.md:319 alternative: every Y_n from the original X */
+    /* Opt-in flag OR-ed into either variant (changes results, so never the
+     * default): Omega_n is the Khatri-Rao product of per-mode Gaussian factors F_{n,m}
+     * (S_m x K_n, m != n, S = the working shape of mode n) instead of prod_{m != n} S_m x K_n
+     * independent draws. The factors are drawn from the same stream `seed`, column-major, in
+     * mode order n, then m, starting at draw 0; skipped modes draw nothing. Supported where the
+     * fp64 streaming kernels run (fp64 tensors with mode extents <= 128 and K_n <= 16). */
+    TRG_OMEGA_KHATRI_RAO = 16
 };
 enum trg_method { TRG_ALS = 0, TRG_SVD = 1 };
 

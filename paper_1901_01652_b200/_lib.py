@@ -33,6 +33,7 @@ EXPORTS = [
 TRG_OK, TRG_EINVAL, TRG_ERANGE, TRG_ECUDA, TRG_ENCCL, TRG_ENUMERIC, TRG_ENODEV = 0, 1, 2, 3, 4, 5, 6
 TRG_F32, TRG_F64 = 0, 1
 TRG_SEQUENTIAL, TRG_FUSED = 0, 1
+TRG_OMEGA_KHATRI_RAO = 16  # flag OR-ed into the variant (trg.h)
 TRG_ALS, TRG_SVD = 0, 1
 
 

@@ -29,6 +29,18 @@ from . import _lib as L
 class ProjectionSpec:
     sketch_dims: List[int]
     seed: int = 0
+    # "gaussian": the reference's i.i.d. test matrices (sketch.hpp:32-38). "khatri_rao": opt-in
+    # structured test matrices, products of per-mode Gaussian factors (trg.h TRG_OMEGA_KHATRI_RAO);
+    # different results, no per-element draws
+    omega: str = "gaussian"
+
+
+def _variant(variant, spec):
+    if spec.omega == "gaussian":
+        return variant
+    if spec.omega == "khatri_rao":
+        return variant | L.TRG_OMEGA_KHATRI_RAO
+    raise ValueError(f"ProjectionSpec.omega must be 'gaussian' or 'khatri_rao', not {spec.omega!r}")
 
 
 @dataclass
@@ -257,8 +269,8 @@ class DeviceSketch:
         if len(self.K) != len(self.dims):
             raise ValueError("sketch: projection size list must match tensor order")
         k, kp = L.i64(self.K)
-        L.call("trg_sketch_run", ctx.handle, x.handle, kp, ctypes.c_uint64(spec.seed), ctypes.c_int(variant),
-               ctypes.byref(self._h))
+        L.call("trg_sketch_run", ctx.handle, x.handle, kp, ctypes.c_uint64(spec.seed),
+               ctypes.c_int(_variant(variant, spec)), ctypes.byref(self._h))
         ctx._adopt(self)
 
     def projected(self):
@@ -503,7 +515,8 @@ def decompose(x, method, cfg, spec, variant=L.TRG_SEQUENTIAL, ctx=None):
         raise ValueError("trals: rank vector length must equal tensor order")
     h = ctypes.c_void_p()
     common = (ctypes.c_int(m), rk[1], ctypes.c_double(cfg.tolerance), ctypes.c_int64(cfg.max_sweeps),
-              ctypes.c_uint64(cfg.seed), kp, ctypes.c_uint64(spec.seed), ctypes.c_int(variant), ctypes.byref(h))
+              ctypes.c_uint64(cfg.seed), kp, ctypes.c_uint64(spec.seed), ctypes.c_int(_variant(variant, spec)),
+              ctypes.byref(h))
     if isinstance(x, DeviceTensor):
         L.call("trg_decompose", ctx.handle, x.handle, *common)
     else:

@@ -11,6 +11,19 @@ enum DType { F32 = 0, F64 = 1 };
 
 inline size_t dtype_size(int dt) { return dt == F64 ? 8 : 4; }
 
+// ---- opt-in Khatri-Rao test matrix (TRG_OMEGA_KHATRI_RAO) ----
+// Omega_n(c, k) = A(c mod left, k) * F(r mod S1, k) * H(r / S1, k), r = c / left, where A is the
+// Khatri-Rao product of the per-mode Gaussian factors of the modes before n (left x K), F the
+// factor of mode n + 1 (S1 x K) and H the product of the factors after n + 1 (nH x K); all
+// column-major fp64, c and r global unfolding indices (runtime.cpp build_kr). F == nullptr: the
+// reference Gaussian stream.
+struct KrOmega {
+    const double* A = nullptr;
+    const double* F = nullptr;
+    const double* H = nullptr;
+    int64_t left = 1, S1 = 1, nH = 1;
+};
+
 // ---- sketch: Y_n = P_(n) * Omega_n (K1), deterministic split-K -------------
 // The current tensor is read as (left, dim, right) (tensor.hpp:112-123);
 // unfold_classic column c = l + left*r (tensor.hpp:133-142). Omega_n(c, k) is
@@ -22,6 +35,7 @@ struct SketchPlan {
     int K;
     uint64_t seed, D;
     int64_t rows_glob, col_off;
+    KrOmega kr;  // Khatri-Rao test matrix instead of the draws (stream / slab kernels only)
     // derived by plan_sketch()
     int TD, TK, Kp, DT, CT, nd, nk, G, threads, ndt;
     int64_t ncols, ntiles;
@@ -101,11 +115,22 @@ struct OmegaUnitsJob {  // one mode's unit blocks, generated by k_omega_units or
     uint64_t seed = 0, D = 0;
     int64_t col_off = 0, rows_glob = 0;
     const GaussTables* gt = nullptr;
+    KrOmega kr;  // kr.F set: the unit blocks of the Khatri-Rao test matrix instead of the draws
 };
 OmegaUnitsJob omega_units_job(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
-                              int64_t rows_glob, double* out);
+                              int64_t rows_glob, double* out, const KrOmega* kr = nullptr);
 void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
-                        int64_t rows_glob, double* out, cudaStream_t s);
+                        int64_t rows_glob, double* out, cudaStream_t s, const KrOmega* kr = nullptr);
+// Khatri-Rao tables in one launch: table t is out(row, k) = prod_j draws[off_j + i_j + rows_j k],
+// row = sum_j i_j stride_j (first index fastest); nf = 0 gives a column of ones.
+constexpr int kKrMaxTables = 24, kKrMaxFactors = 7;
+struct KrTable {
+    double* out;
+    int64_t nrows;
+    int K, nf;
+    int64_t off[kKrMaxFactors], rows[kKrMaxFactors];
+};
+void launch_kr_tables(const double* draws, const KrTable* tabs, int ntab, cudaStream_t s);
 // standard-layout test matrix (rows left*right, K columns) -> unit blocks
 void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s);
 int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,

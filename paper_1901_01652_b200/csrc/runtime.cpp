@@ -392,9 +392,10 @@ struct YParts {
 
 void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
                  int n, int64_t Kn, uint64_t seed, const ModeOffsets& off, double* dYfull, PreOmega* pre = nullptr,
-                 YParts* yp = nullptr) {
+                 YParts* yp = nullptr, const trg::KrOmega* kr = nullptr) {
     const int N = (int)cur_shape.size();
     trg::SketchPlan p{};
+    if (kr) p.kr = *kr;
     p.dtype = cdt;
     p.left = prod(cur_shape, 0, n);
     p.dim = cur_shape[n];
@@ -411,6 +412,10 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     static const bool no_fuse_qr = getenv("TRG_QR_LEGACY") != nullptr;
     const bool defer = yp && ctx->world == 1 && !no_fuse_qr && trg::qr_fused_ok(p.dim, (int)Kn);
     double* yout = defer ? nullptr : ylocal;
+    const bool slab2 = p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right);
+    require(!kr || trg::stream_sketch_ok(p.dtype, p.left, p.dim, (int)Kn) || slab2,
+            "sketch: the Khatri-Rao test matrix needs the fp64 streaming kernels for mode " + std::to_string(n) +
+                " (fp64 working tensor, mode extent <= 128, K <= 16; build_kr)");
     if (trg::stream_sketch_ok(p.dtype, p.left, p.dim, (int)Kn)) {
         partial = (double*)ctx->tmp(sizeof(double) * ctx->num_sms * p.dim * Kn);
         int grid = 0;
@@ -426,7 +431,7 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
             gc = trg::launch_stream_sketch_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
         }, yout ? 2 : 1);
         if (defer) *yp = YParts{partial, gc};
-    } else if (p.left > 1 && trg::slab2_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+    } else if (slab2) {
         const int NT = Kn <= 8 ? 1 : 2;
         double* om = nullptr;
         const bool have = pre && pre->buf;
@@ -435,7 +440,7 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
         if (!have || pre->pending) {  // no earlier launch generated the blocks: do it here
             ctx->launch("omega_m" + std::to_string(n), [&] {
                 trg::launch_omega_units(p.left, p.right, (int)Kn, p.seed, p.D, p.col_off, p.rows_glob, om,
-                                        ctx->stream);
+                                        ctx->stream, kr);
             });
             if (have) pre->pending = false;
         }
@@ -518,7 +523,7 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
 // them on their idle CTAs (launch_qr_fused), or the sketch of that mode does if none could
 void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const std::vector<int64_t>& K, uint64_t seed,
                         const std::vector<ModeOffsets>& offs, int after, std::vector<PreOmega>& pre,
-                        bool in_launch = false) {
+                        bool in_launch = false, const std::vector<trg::KrOmega>* kr = nullptr) {
     const int N = (int)x->dims.size();
     std::vector<int64_t> shape = x->local_shape();
     for (int m = 0; m <= after; ++m) shape[m] = K[m];
@@ -533,7 +538,7 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const s
             pre[m].buf = (double*)ctx->tmp(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
             if (in_launch) {
                 pre[m].job = trg::omega_units_job(left, right, (int)K[m], seed, offs[m].D, offs[m].col_off,
-                                                  offs[m].rows_glob, pre[m].buf);
+                                                  offs[m].rows_glob, pre[m].buf, kr ? &(*kr)[m] : nullptr);
                 pre[m].pending = true;
                 shape[m] = K[m];
                 continue;
@@ -541,7 +546,7 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const s
             CK(cudaEventRecord(go, ctx->stream));
             CK(cudaStreamWaitEvent(ctx->side, go, 0));
             trg::launch_omega_units(left, right, (int)K[m], seed, offs[m].D, offs[m].col_off, offs[m].rows_glob,
-                                    pre[m].buf, ctx->side);
+                                    pre[m].buf, ctx->side, kr ? &(*kr)[m] : nullptr);
             CK(cudaGetLastError());
             ctx->launches += 1;
             CK(cudaEventCreateWithFlags(&pre[m].ready, cudaEventDisableTiming));
@@ -704,10 +709,107 @@ void run_sketch_deferred(trg_ctx* ctx, const trg_tensor* x, uint64_t seed, trg_s
     sk->P_is_view = false;
 }
 
+// ------------------------------------------------------------------ Khatri-Rao test matrices (f4)
+// Omega_n(c, k) = prod_{m != n} F_{n,m}(i_m, k) for unfolding column c = sum_{m != n} i_m stride_m
+// (first index fastest), F_{n,m} an S_m x K_n block of the stream `seed` (trg.h
+// TRG_OMEGA_KHATRI_RAO for the draw order). The kernels take it as A(c mod left) F(r mod S1)
+// H(r / S1) with r = c / left (kernels.h KrOmega): A and H are materialised (at most
+// prod_{m < n} S_m and prod_{m > n + 1} S_m rows), F is the factor of mode n + 1 itself.
+struct KrPlan {
+    std::vector<trg::KrOmega> om;  // per mode (F == nullptr for skipped modes)
+    std::vector<void*> bufs;       // device buffers, freed stream-ordered after the run
+};
+
+KrPlan build_kr(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t seed, int variant) {
+    const int N = (int)x->dims.size();
+    const std::vector<int64_t>& dims = x->dims;
+    {  // every projected mode must take a kernel with the Khatri-Rao entries (before any launch)
+        std::vector<int64_t> shape = x->local_shape();
+        const int cdt = x->dtype;
+        for (int n = 0; n < N; ++n) {
+            if (K[n] == dims[n]) continue;
+            const int64_t left = prod(shape, 0, n), dim = shape[n], right = prod(shape, n + 1);
+            require(trg::stream_sketch_ok(cdt, left, dim, (int)K[n]) ||
+                        (left > 1 && trg::slab2_ok(cdt, left, dim, K[n], right)),
+                    "sketch: the Khatri-Rao test matrix needs the fp64 streaming kernels for mode " +
+                        std::to_string(n) + " (fp64 tensor, mode extent <= 128, K_n <= 16)");
+            if (variant == TRG_SEQUENTIAL) shape[n] = K[n];
+        }
+    }
+    KrPlan kp;
+    kp.om.resize(N);
+    std::vector<std::vector<int64_t>> S(N), off(N);
+    int64_t total = 0;
+    for (int n = 0; n < N; ++n) {
+        if (K[n] == dims[n]) continue;
+        S[n].resize(N);
+        off[n].assign(N, -1);
+        for (int m = 0; m < N; ++m) S[n][m] = (m < n && variant == TRG_SEQUENTIAL) ? K[m] : dims[m];
+        for (int m = 0; m < N; ++m)
+            if (m != n) {
+                off[n][m] = total;
+                total += S[n][m] * K[n];
+            }
+    }
+    if (total == 0) return kp;
+    // the factor draws (one launch), then every table of every mode (one launch)
+    std::vector<trg::KrTable> tabs;
+    int64_t elems = 0;
+    for (int n = 0; n < N; ++n) {
+        if (K[n] == dims[n]) continue;
+        // Khatri-Rao product of the factors of modes [m0, m1) other than n
+        auto table = [&](int m0, int m1, int64_t* nrows) {
+            trg::KrTable t{};
+            t.K = (int)K[n];
+            t.nrows = 1;
+            for (int m = m0; m < m1; ++m)
+                if (m != n) {
+                    require(t.nf < trg::kKrMaxFactors, "sketch: Khatri-Rao supports tensors of order <= 8");
+                    t.off[t.nf] = off[n][m];
+                    t.rows[t.nf++] = S[n][m];
+                    t.nrows *= S[n][m];
+                }
+            t.out = reinterpret_cast<double*>(elems);  // element offset for now, pointer below
+            elems += t.nrows * t.K;
+            tabs.push_back(t);
+            *nrows = t.nrows;
+            return t.out;
+        };
+        trg::KrOmega& o = kp.om[n];
+        o.A = table(0, n, &o.left);
+        if (n + 1 < N) {
+            o.F = table(n + 1, n + 2, &o.S1);
+            o.H = table(n + 2, N, &o.nH);
+        } else {
+            o.F = o.H = table(N, N, &o.nH);  // one row of ones
+            o.S1 = 1;
+        }
+        require(o.S1 * o.nH < (int64_t(1) << 32), "sketch: Khatri-Rao row index beyond 32 bits");
+    }
+    double* draws = (double*)ctx->alloc(sizeof(double) * (total + elems));
+    double* base = draws + total;
+    kp.bufs.push_back(draws);
+    trg::launch_omega(seed, 0, total, 1, draws, ctx->stream);
+    auto rebase = [&](const double* off_as_ptr) { return base + reinterpret_cast<intptr_t>(off_as_ptr); };
+    for (auto& t : tabs) t.out = const_cast<double*>(rebase(t.out));
+    for (int n = 0; n < N; ++n)
+        if (K[n] != dims[n]) {  // (the first table sits at offset 0, i.e. "nullptr" until here)
+            trg::KrOmega& o = kp.om[n];
+            o.A = rebase(o.A);
+            o.F = rebase(o.F);
+            o.H = rebase(o.H);
+        }
+    trg::launch_kr_tables(draws, tabs.data(), (int)tabs.size(), ctx->stream);
+    ctx->launches += 2;
+    return kp;
+}
+
 void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk,
                 bool allow_deferred = true) {
     const int N = (int)x->dims.size();
     validate_K(x, Kin);
+    const bool kr_on = (variant & TRG_OMEGA_KHATRI_RAO) != 0;
+    variant &= ~TRG_OMEGA_KHATRI_RAO;
     require(variant == TRG_SEQUENTIAL || variant == TRG_FUSED, "sketch: unknown variant");
     sk->ctx = ctx;
     sk->dtype = x->dtype;
@@ -723,7 +825,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 3 * N, ctx->stream));
     sk->x = x;
     sk->seed = seed;
-    if (allow_deferred && deferred_eligible(ctx, x, Kin, variant)) {
+    if (allow_deferred && !kr_on && deferred_eligible(ctx, x, Kin, variant)) {
         sk->deferred = true;
         sk->checked = false;
         run_sketch_deferred(ctx, x, seed, sk);
@@ -732,6 +834,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     }
     sk->deferred = false;
     sk->checked = true;
+    const KrPlan krp = kr_on ? build_kr(ctx, x, Kin, seed, variant) : KrPlan{};
+    auto krn = [&](int n) { return kr_on ? &krp.om[n] : nullptr; };
     ctx->scr_begin();
 
     int cdt = x->dtype;  // dtype of the working tensor (fp32 input is promoted by its mode-0 shrink)
@@ -784,7 +888,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
-            if (!y_ready[n]) sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n]);
+            if (!y_ready[n])
+                sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n], krn(n));
             static const bool side_omega = getenv("TRG_SIDE_OMEGA") != nullptr;
             if (!pre_started && yparts[n].partial && !side_omega) {
                 // ticketed QR launches: their CTAs past the reduce generate the later test
@@ -792,7 +897,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 // HBM-bound shrink
                 pre_started = true;
                 const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
-                schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre, true);
+                schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre, true,
+                                   kr_on ? &krp.om : nullptr);
             }
             qr(n);
             if (!pre_started) {
@@ -802,7 +908,8 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 // the sketch, which it would slow down
                 pre_started = true;
                 const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
-                schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre);
+                schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre, false,
+                                   kr_on ? &krp.om : nullptr);
             }
             const bool join_after_shrink = n == first_proj;
             void* out = nullptr;
@@ -810,7 +917,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
             // K3: fuse this shrink with the next mode's sketch while P^(1) tiles are on chip
             // off by default: the separate shrink + TMA slab sketch measure faster (profiles/)
             static const bool fuse = getenv("TRG_FUSE") != nullptr;
-            if (fuse && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
+            if (fuse && !kr_on && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
                 trg::fused_ttm_sketch_ok(cdt, 1, shape[0], Kn, shape[1], sk->K[1])) {
                 trg::FusedPlan fp{};
                 fp.I0 = shape[0];
@@ -864,7 +971,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;
-            sketch_mode(ctx, x, x->dtype, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n], nullptr, &yparts[n]);
+            sketch_mode(ctx, x, x->dtype, x->d, xshape, n, Kn, seed, offs[n], sk->dY[n], nullptr, &yparts[n], krn(n));
             qr(n);
         }
         for (int n = 0; n < N; ++n) {
@@ -918,6 +1025,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     }
     for (auto& po : pre)
         if (po.ready) cudaEventDestroy(po.ready);  // destruction is deferred until the event completes
+    for (void* b : krp.bufs) ctx->dfree(b);  // stream-ordered: after the last kernel that reads them
     ctx->scr_end();
     CK(cudaEventRecord(sk->ev1, ctx->stream));
 }

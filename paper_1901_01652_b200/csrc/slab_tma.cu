@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <stdexcept>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -92,6 +93,31 @@ struct Slab2Args {
 
 // ------------------------------------------------------------------ test-matrix unit blocks
 // (omega_units.cuh)
+struct KrTables {
+    KrTable t[kKrMaxTables];
+    int64_t start[kKrMaxTables + 1];  // prefix sums of nrows * K
+    int n;
+};
+
+__global__ void k_kr_tables(const double* __restrict__ draws, KrTables T) {
+    const int64_t total = T.start[T.n];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int ti = 0;
+        while (e >= T.start[ti + 1]) ++ti;
+        const KrTable& tb = T.t[ti];
+        const int64_t le = e - T.start[ti];
+        const int64_t k = le / tb.nrows;
+        int64_t row = le - k * tb.nrows;
+        double v = 1.0;
+        for (int j = 0; j < tb.nf; ++j) {
+            const int64_t q = row / tb.rows[j];
+            v *= draws[tb.off[j] + (row - q * tb.rows[j]) + tb.rows[j] * k];
+            row = q;
+        }
+        tb.out[le] = v;
+    }
+}
+
 __global__ void k_omega_units(OmegaUnitsJob j) {
     __shared__ GaussTables tabs;
     gauss_tables_to_smem(tabs, j.gt);
@@ -435,9 +461,26 @@ bool slab2_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right) {
 
 int64_t slab2_units(int64_t left, int64_t right) { return right * ((left + kUnitL - 1) / kUnitL); }
 
+void launch_kr_tables(const double* draws, const KrTable* tabs, int ntab, cudaStream_t s) {
+    if (ntab > kKrMaxTables) throw std::runtime_error("khatri_rao: too many factor tables");
+    KrTables T{};
+    T.n = ntab;
+    T.start[0] = 0;
+    for (int i = 0; i < ntab; ++i) {
+        if (tabs[i].nf > kKrMaxFactors) throw std::runtime_error("khatri_rao: too many factors per table");
+        T.t[i] = tabs[i];
+        T.start[i + 1] = T.start[i] + tabs[i].nrows * tabs[i].K;
+    }
+    const int64_t n = T.start[ntab];
+    if (n == 0) return;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_kr_tables<<<blocks, 256, 0, s>>>(draws, T);
+}
+
 OmegaUnitsJob omega_units_job(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
-                              int64_t rows_glob, double* out) {
+                              int64_t rows_glob, double* out, const KrOmega* kr) {
     OmegaUnitsJob j;
+    if (kr) j.kr = *kr;
     j.out = out;
     j.left = left;
     j.LC = (int)((left + kUnitL - 1) / kUnitL);
@@ -452,10 +495,11 @@ OmegaUnitsJob omega_units_job(int64_t left, int64_t right, int K, uint64_t seed,
 }
 
 void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint64_t D, int64_t col_off,
-                        int64_t rows_glob, double* out, cudaStream_t s) {
-    OmegaUnitsJob j = omega_units_job(left, right, K, seed, D, col_off, rows_glob, out);
+                        int64_t rows_glob, double* out, cudaStream_t s, const KrOmega* kr) {
+    OmegaUnitsJob j = omega_units_job(left, right, K, seed, D, col_off, rows_glob, out, kr);
     j.gt = gauss_tables(s);
-    const int threads = (omega_unit_slots(j.NT) + 31) & ~31;  // one unit per iteration, zeros included
+    // one unit per iteration, zeros included (Khatri-Rao: one thread per block element)
+    const int threads = j.kr.F ? 4 * j.NT * 32 : (omega_unit_slots(j.NT) + 31) & ~31;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(j.nunits, 148 * 12));
     k_omega_units<<<blocks, threads, 0, s>>>(j);
 }

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "launch.h"
+#include "omega_units.cuh"
 #include "pipeline.cuh"
 
 namespace trg {
@@ -63,6 +64,8 @@ struct SkArgs {
     double* partial;
     const GaussTables* gt;
     int pol;  // L2 policy of the X reads (policy_l2)
+    KrOmega kr;  // kr.F set: Khatri-Rao test matrix (left = 1: Omega(c, k) = B(col_off + c, k))
+    int kr_smem; // F (S1 x K) staged in shared memory after the barriers (sk_plan headroom)
 };
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
@@ -133,7 +136,8 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     // even draw (then nothing is wasted), one more otherwise. The fast path (even starts, one
     // round of the generator threads covers a tile) gives each thread one fixed (column, pair)
     // slot; a tile is then written by nitems threads.
-    const bool odd = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) != 0;
+    const bool kr = a.kr.F != nullptr;  // Khatri-Rao entries have no draw-pair parity
+    const bool odd = !kr && ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) != 0;
     const int npmax = odd ? CT / 2 + 1 : CT / 2;
     const int nitems = a.K * npmax;
     // fast-path slots: a warp's 32 slots cover 8 columns x 4 row pairs of one 32-row block of the
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
             const uint64_t gam = 0x9E3779B97F4A7C15ull;
             const uint64_t inc = (uint64_t)gridDim.x * (uint64_t)CT * gam;  // one tile of this CTA
             uint64_t st[kIpt];
-            int o0[kIpt], c0[kIpt];
+            int o0[kIpt], c0[kIpt], kk[kIpt];
             bool on[kIpt];
 #pragma unroll
             for (int i = 0; i < kIpt; ++i) {
@@ -210,12 +214,71 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                 const int jj = on[i] ? jq : 0;
                 o0[i] = omega_idx(2 * jj, k, NT);  // row 2jj + 1 is the next double (2jj even)
                 c0[i] = 2 * jj;
+                kk[i] = k;
                 const uint64_t p0 = ((a.D + (uint64_t)a.col_off +
                                       ((uint64_t)blockIdx.x + (uint64_t)sub * gridDim.x) * CT +
                                       (uint64_t)a.rows_glob * (uint64_t)k) >> 1) + (uint64_t)jj;
                 st[i] = a.seed + (2ull * p0 + 1ull) * gam;
             }
             const int64_t full_tiles = a.ncols / CT;  // tiles t < full_tiles have all CT columns
+            if (kr && a.kr_smem && kIlp == 1) {
+                // Khatri-Rao entries F(i1, k) H(q, k), c = i1 + S1 q: F from shared memory, H(q, k)
+                // and H(q + 1, k) loaded one tile ahead; i1 and q advance by constants per tile
+                double* Fs = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(bars) + kBarBytes);
+                const int S1 = (int)a.kr.S1;
+                for (int e = rt; e < S1 * a.K; e += nslots <= nth ? R * nslots : nth) Fs[e] = a.kr.F[e];
+                const int ngen = nslots <= nth ? R * nslots : nth;  // generator threads past `sub >= R`
+                asm volatile("bar.sync 2, %0;" ::"r"(ngen) : "memory");
+                const int64_t step_c = (int64_t)R * gridDim.x * CT;  // columns from one tile of a thread to its next
+                const int di = (int)(step_c % S1);
+                const int64_t dq = step_c / S1;
+                int i1[kIpt];
+                int64_t qq[kIpt];
+                double h0[kIpt], h1[kIpt];
+#pragma unroll
+                for (int i = 0; i < kIpt; ++i) {
+                    const int64_t c = a.col_off + ((int64_t)blockIdx.x + (int64_t)sub * gridDim.x) * CT + c0[i];
+                    qq[i] = c / S1;
+                    i1[i] = (int)(c - qq[i] * S1);
+                    const double* hk = a.kr.H + a.kr.nH * kk[i];
+                    h0[i] = qq[i] < a.kr.nH ? __ldg(hk + qq[i]) : 0.0;
+                    h1[i] = qq[i] + 1 < a.kr.nH ? __ldg(hk + qq[i] + 1) : 0.0;
+                }
+                int bx = sub % nob, bp = (sub / nob) & 1;
+                for (int j = sub; j < nl; j += R) {
+                    mbar_wait(&empty_o[bx], bp ^ 1);
+                    double z[kIpt][2];
+#pragma unroll
+                    for (int i = 0; i < kIpt; ++i) {
+                        const double* fk = Fs + S1 * kk[i];
+                        z[i][0] = fk[i1[i]] * h0[i];
+                        z[i][1] = i1[i] + 1 < S1 ? fk[i1[i] + 1] * h0[i] : fk[0] * h1[i];
+                        i1[i] += di;
+                        qq[i] += dq;
+                        if (i1[i] >= S1) {
+                            i1[i] -= S1;
+                            qq[i] += 1;
+                        }
+                        const double* hk = a.kr.H + a.kr.nH * kk[i];  // next tile's H entries, in flight
+                        h0[i] = qq[i] < a.kr.nH ? __ldg(hk + qq[i]) : 0.0;
+                        h1[i] = qq[i] + 1 < a.kr.nH ? __ldg(hk + qq[i] + 1) : 0.0;
+                    }
+                    double* O = omega + bx * omega_elems;
+                    const int64_t ncol = a.ncols - (blockIdx.x + (int64_t)j * gridDim.x) * CT;
+#pragma unroll
+                    for (int i = 0; i < kIpt; ++i)
+                        if (on[i])
+                            *reinterpret_cast<double2*>(O + o0[i]) =
+                                make_double2(c0[i] < ncol ? z[i][0] : 0.0, c0[i] + 1 < ncol ? z[i][1] : 0.0);
+                    mbar_arrive(&full_o[bx]);
+                    bx += R;
+                    if (bx >= nob) {
+                        bx -= nob;
+                        bp ^= 1;
+                    }
+                }
+                return;
+            }
             // local tiles jt < jfull are full; buffer index and phase of tile j + u R advance by G
             const int64_t jf = (full_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
             const int jfull = jf > 0 ? (int)jf : 0;
@@ -240,7 +303,15 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
 #ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
                         z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
 #else
-                        gauss_pair_state(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0], z[u][i][1]);
+                        if (kr) {  // products of the factor entries (L1-resident): no draws at all
+                            const int64_t cl = (blockIdx.x + (int64_t)(j + u * R) * gridDim.x) * CT + c0[i];
+                            const uint32_t cg = (uint32_t)(a.col_off + cl);
+                            z[u][i][0] = on[i] && cl < a.ncols ? kr_b(a.kr, cg, kk[i]) : 0.0;
+                            z[u][i][1] = on[i] && cl + 1 < a.ncols ? kr_b(a.kr, cg + 1u, kk[i]) : 0.0;
+                        } else {
+                            gauss_pair_state(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0],
+                                             z[u][i][1]);
+                        }
 #endif
                     }
 #pragma unroll
@@ -298,7 +369,15 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                     const uint64_t p = (s0 >> 1) + (uint64_t)jj;
                     live[u] = u < ntl && p <= ((s0 + (uint64_t)CT - 1ull) >> 1);
                     cc[u] = (int64_t)(2ull * p - s0);
-                    gauss_pair_tab(a.seed, live[u] ? p : 0ull, *tabs, z[u][0], z[u][1]);
+                    if (kr) {  // rows 2 jj, 2 jj + 1 of the tile (no parity offset)
+                        cc[u] = 2 * jj;
+                        live[u] = u < ntl && 2 * jj < CT;
+                        const int64_t cl = c0 + cc[u];
+                        z[u][0] = live[u] && cl < a.ncols ? kr_b(a.kr, (uint32_t)(a.col_off + cl), k) : 0.0;
+                        z[u][1] = live[u] && cl + 1 < a.ncols ? kr_b(a.kr, (uint32_t)(a.col_off + cl + 1), k) : 0.0;
+                    } else {
+                        gauss_pair_tab(a.seed, live[u] ? p : 0ull, *tabs, z[u][0], z[u][1]);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < kIlp; ++u) {
@@ -905,9 +984,15 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     a.D = p.D;
     a.partial = partial;
     a.gt = gauss_tables(s);
+    a.kr = p.kr;
+    a.kr_smem = 0;
+    size_t smem = pl.smem;
+    if (p.kr.F && smem + (size_t)p.kr.S1 * p.K * 8 <= 227 * 1024 && p.kr.S1 <= (1 << 20)) {
+        a.kr_smem = 1;
+        smem += (size_t)p.kr.S1 * p.K * 8;  // F in the headroom of the stage plan
+    }
     const int NT = nt_for(p.K);
     const int mtw = sk_mtw(p.dim);
-    const size_t smem = pl.smem;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     *grid_out = grid;
     const int threads = (kSkCons + kRng + 1) * 32;

@@ -146,6 +146,61 @@ def sketch(x, K, seed, variant=0):
     return proj.reshape(tuple(K), order="F"), outb, outy
 
 
+def kr_factor_layout(dims, K, variant=0):
+    """Draw layout of the opt-in Khatri-Rao test matrices (include/trg.h TRG_OMEGA_KHATRI_RAO):
+    per projected mode n, the factors F_{n,m} (m != n, ascending) of S_m x K_n draws, column-major,
+    consecutive in the stream from draw 0; S = the working shape of mode n (K_m for m < n in the
+    sequential variant, I_m otherwise). Returns ({n: {m: (offset, S_m)}}, total draws)."""
+    layout, total = {}, 0
+    for n, (I, Kn) in enumerate(zip(dims, K)):
+        if Kn == I:
+            continue
+        layout[n] = {}
+        for m in range(len(dims)):
+            if m == n:
+                continue
+            S = K[m] if (m < n and variant == 0) else dims[m]
+            layout[n][m] = (total, S)
+            total += S * Kn
+    return layout, total
+
+
+def kr_omega(draws, layout_n, Kn):
+    """Omega_n(c, k) = prod_m F_{n,m}(i_m, k), c = sum_m i_m stride_m (first index fastest)."""
+    cols = []
+    for k in range(Kn):
+        v = np.ones(1)
+        for m in sorted(layout_n):
+            off, S = layout_n[m]
+            f = draws[off:off + S * Kn].reshape((S, Kn), order="F")[:, k]
+            v = np.kron(f, v)  # mode m varies slower than the modes before it
+        cols.append(v)
+    return np.stack(cols, axis=1)
+
+
+def kr_sketch(x, K, seed, variant=0):
+    """The projection of sketch() with Khatri-Rao test matrices: returns (projected, bases, ys)."""
+    x = np.asarray(x, dtype=np.float64)
+    dims, N = list(x.shape), x.ndim
+    layout, total = kr_factor_layout(dims, K, variant)
+    draws = gaussian(seed, total) if total else np.zeros(0)
+    bases = [np.eye(I) for I in dims]
+    ys = [np.zeros((I, Kn)) for I, Kn in zip(dims, K)]
+    P = x.copy()
+    for n in range(N):
+        if n not in layout:
+            continue
+        src = P if variant == 0 else x
+        ys[n] = unfold(src, n) @ kr_omega(draws, layout[n], K[n])
+        bases[n] = economy_q(ys[n])
+        if variant == 0:
+            P = mode_n_product(P, n, bases[n].T)
+    if variant != 0:
+        for n in layout:
+            P = mode_n_product(P, n, bases[n].T)
+    return P, bases, ys
+
+
 def lift_back(projected, bases):
     projected = np.asarray(projected, dtype=np.float64)
     K = projected.shape

@@ -370,3 +370,21 @@ def test_gaussian_seek_equals_sequential_stream():
         full = orc.gaussian(seed, 2000)
         for skip in (0, 1, 2, 7, 998, 1995):
             np.testing.assert_array_equal(orc.gaussian(seed, 5, skip=skip), full[skip:skip + 5])
+
+
+def test_kr_omega_layout_matches_definition():
+    # Omega_n(c, k) = prod_{m != n} F_{n,m}(i_m, k), c first-index-fastest over the other modes,
+    # factors drawn consecutively (include/trg.h TRG_OMEGA_KHATRI_RAO)
+    dims, K = [3, 4, 5], [2, 3, 2]
+    layout, total = orc.kr_factor_layout(dims, K, variant=0)
+    assert total == (4 + 5) * 2 + (2 + 5) * 3 + (2 + 3) * 2 and sorted(layout) == [0, 1, 2]
+    draws = orc.gaussian(9, total)
+    om1 = orc.kr_omega(draws, layout[1], K[1])  # rows (i0 < K0 = 2) x (i2 < 5)
+    f0 = draws[layout[1][0][0]:][:2 * 3].reshape((2, 3), order="F")
+    f2 = draws[layout[1][2][0]:][:5 * 3].reshape((5, 3), order="F")
+    for i0 in range(2):
+        for i2 in range(5):
+            np.testing.assert_array_equal(om1[i0 + 2 * i2], f0[i0] * f2[i2])
+    # fused variant: factors sized by the original extents
+    layout_f, total_f = orc.kr_factor_layout(dims, K, variant=1)
+    assert layout_f[1][0][1] == 3 and total_f == (4 + 5) * 2 + (3 + 5) * 3 + (3 + 4) * 2
