@@ -165,9 +165,14 @@ private:
     std::vector<DenseTensor> cores_;
 };
 
+/// Test matrices: the reference's Gaussian draws, or the opt-in Khatri-Rao products of per-mode
+/// Gaussian factors (trg.h TRG_OMEGA_KHATRI_RAO; different results, no per-element draws).
+enum class Omega { Gaussian = 0, KhatriRao = TRG_OMEGA_KHATRI_RAO };
+
 struct ProjectionSpec {  // sketch.hpp:18-21
     std::vector<index_t> sketch_dims;
     std::uint64_t seed = 0;
+    Omega omega = Omega::Gaussian;  // extension
 };
 
 struct SketchResult {  // sketch.hpp:25-28
@@ -254,7 +259,8 @@ inline SketchResult sketch(const DeviceTensor& x, const std::vector<index_t>& di
                            Context& ctx = default_context(), Variant variant = Variant::Sequential) {
     detail::require(spec.sketch_dims.size() == dims.size(), "sketch: projection size list must match tensor order");
     trg_sketch* sk = nullptr;
-    detail::check(trg_sketch_run(ctx.get(), x.get(), spec.sketch_dims.data(), spec.seed, static_cast<int>(variant), &sk));
+    detail::check(trg_sketch_run(ctx.get(), x.get(), spec.sketch_dims.data(), spec.seed,
+                                 static_cast<int>(variant) | static_cast<int>(spec.omega), &sk));
     std::unique_ptr<trg_sketch, int (*)(trg_sketch*)> guard(sk, trg_sketch_destroy);
     SketchResult out;
     out.projected = DenseTensor(spec.sketch_dims);
@@ -338,7 +344,8 @@ inline SolveReport decompose(const DenseTensor& x, const std::optional<std::vect
     const int N = static_cast<int>(x.order());
     detail::check(trg_decompose_host(ctx.get(), TRG_F64, N, x.shape().data(), x.data(), static_cast<int>(method),
                                      ranks ? ranks->data() : nullptr, cfg.tolerance, cfg.max_sweeps, cfg.seed,
-                                     spec.sketch_dims.data(), spec.seed, static_cast<int>(variant), &h));
+                                     spec.sketch_dims.data(), spec.seed,
+                                     static_cast<int>(variant) | static_cast<int>(spec.omega), &h));
     return detail::report_from(h, x.shape());
 }
 

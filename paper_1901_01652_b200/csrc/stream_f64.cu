@@ -112,7 +112,9 @@ __device__ __forceinline__ void sk_consume(double (&acc)[MTW][NT][2], const doub
     }
 }
 
-template <int MTW, int NT>
+// KR: Khatri-Rao test matrix (a.kr). A separate instantiation, so the branch does not perturb the
+// Gaussian generator's code (sharing one instantiation cost the Gaussian path 17 us on C2).
+template <int MTW, int NT, bool KR>
 __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(SkArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SK_T(k0);
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
     // even draw (then nothing is wasted), one more otherwise. The fast path (even starts, one
     // round of the generator threads covers a tile) gives each thread one fixed (column, pair)
     // slot; a tile is then written by nitems threads.
-    const bool kr = a.kr.F != nullptr;  // Khatri-Rao entries have no draw-pair parity
+    constexpr bool kr = KR;  // Khatri-Rao entries have no draw-pair parity
     const bool odd = !kr && ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) != 0;
     const int npmax = odd ? CT / 2 + 1 : CT / 2;
     const int nitems = a.K * npmax;
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                 st[i] = a.seed + (2ull * p0 + 1ull) * gam;
             }
             const int64_t full_tiles = a.ncols / CT;  // tiles t < full_tiles have all CT columns
-            if (kr && a.kr_smem && kIlp == 1) {
+            if (kr && a.kr_smem && kIlp == 1) {  // (kr is a template constant: compiled out for Gaussian)
                 // Khatri-Rao entries F(i1, k) H(q, k), c = i1 + S1 q: F from shared memory, H(q, k)
                 // and H(q + 1, k) loaded one tile ahead; i1 and q advance by constants per tile
                 double* Fs = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(bars) + kBarBytes);
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
 #ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
                         z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
 #else
-                        if (kr) {  // products of the factor entries (L1-resident): no draws at all
+                        if constexpr (kr) {  // products of the factor entries (L1-resident): no draws
                             const int64_t cl = (blockIdx.x + (int64_t)(j + u * R) * gridDim.x) * CT + c0[i];
                             const uint32_t cg = (uint32_t)(a.col_off + cl);
                             z[u][i][0] = on[i] && cl < a.ncols ? kr_b(a.kr, cg, kk[i]) : 0.0;
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                     const uint64_t p = (s0 >> 1) + (uint64_t)jj;
                     live[u] = u < ntl && p <= ((s0 + (uint64_t)CT - 1ull) >> 1);
                     cc[u] = (int64_t)(2ull * p - s0);
-                    if (kr) {  // rows 2 jj, 2 jj + 1 of the tile (no parity offset)
+                    if constexpr (kr) {  // rows 2 jj, 2 jj + 1 of the tile (no parity offset)
                         cc[u] = 2 * jj;
                         live[u] = u < ntl && 2 * jj < CT;
                         const int64_t cl = c0 + cc[u];
@@ -998,8 +1000,13 @@ void launch_stream_sketch(const SketchPlan& p, const void* x, double* partial, d
     const int threads = (kSkCons + kRng + 1) * 32;
 #define TRG_SK(MTW, NTV)                                                 \
     do {                                                                 \
-        set_smem(k_sketch_l1_f64<MTW, NTV>, smem);                       \
-        pdl_launch(k_sketch_l1_f64<MTW, NTV>, dim3(grid), dim3(threads), smem, s, a); \
+        if (a.kr.F) {                                                    \
+            set_smem(k_sketch_l1_f64<MTW, NTV, true>, smem);             \
+            pdl_launch(k_sketch_l1_f64<MTW, NTV, true>, dim3(grid), dim3(threads), smem, s, a); \
+        } else {                                                         \
+            set_smem(k_sketch_l1_f64<MTW, NTV, false>, smem);            \
+            pdl_launch(k_sketch_l1_f64<MTW, NTV, false>, dim3(grid), dim3(threads), smem, s, a); \
+        }                                                                \
     } while (0)
 #define TRG_SK_NT(MTW)                   \
     switch (NT) {                        \
