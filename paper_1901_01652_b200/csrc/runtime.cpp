@@ -1295,7 +1295,10 @@ trg_tensor* tensor_new(trg_ctx* ctx, int dtype, int order, const int64_t* dims) 
     require(t->hi > t->lo, "tensor: last mode extent smaller than the number of ranks");
     t->local_elems = t->inner() * (t->hi - t->lo);
     CK(cudaSetDevice(ctx->device));
-    CK(cudaMalloc(&t->d, trg::dtype_size(dtype) * (size_t)t->local_elems));
+    // from the context's stream-ordered pool (release threshold: keep), so repeated
+    // create/destroy (trg_decompose_host per call) costs no driver allocation or implicit sync
+    CK(cudaMallocAsync(&t->d, trg::dtype_size(dtype) * (size_t)t->local_elems, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // usable from any stream on return
     return t.release();
 }
 
@@ -1547,8 +1550,8 @@ int trg_tensor_synthesize(trg_tensor* t, const int64_t* ranks, const double* cor
 int trg_tensor_destroy(trg_tensor* t) {
     return guard([&] {
         if (!t) return;
+        cudaFreeAsync(t->d, t->ctx->stream);  // after the context's work on it; pool-owned memory
         cudaStreamSynchronize(t->ctx->stream);
-        cudaFree(t->d);
         delete t;
     });
 }
