@@ -18,7 +18,7 @@ FULL_METRICS = [
     ("gpu__time_duration.sum", "us"),
     ("dram__bytes_read.sum", "MB rd"),
     ("dram__bytes_write.sum", "MB wr"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %pk"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %pk"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %pk"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ %"),
