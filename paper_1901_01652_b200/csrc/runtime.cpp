@@ -754,10 +754,16 @@ KrPlan build_kr(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t se
     if (total == 0) return kp;
     // the factor draws (one launch), then every table of every mode (one launch)
     std::vector<trg::KrTable> tabs;
+    // table layout first (element offsets into one buffer after the draws), pointers after the
+    // single allocation
+    struct Slot {
+        int64_t a, f, h;  // element offsets of A, F, H
+    };
+    std::vector<Slot> slot(N);
     int64_t elems = 0;
     for (int n = 0; n < N; ++n) {
         if (K[n] == dims[n]) continue;
-        // Khatri-Rao product of the factors of modes [m0, m1) other than n
+        // Khatri-Rao product of the factors of modes [m0, m1) other than n; returns its offset
         auto table = [&](int m0, int m1, int64_t* nrows) {
             trg::KrTable t{};
             t.K = (int)K[n];
@@ -769,19 +775,19 @@ KrPlan build_kr(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t se
                     t.rows[t.nf++] = S[n][m];
                     t.nrows *= S[n][m];
                 }
-            t.out = reinterpret_cast<double*>(elems);  // element offset for now, pointer below
-            elems += t.nrows * t.K;
             tabs.push_back(t);
             *nrows = t.nrows;
-            return t.out;
+            const int64_t at = elems;
+            elems += t.nrows * t.K;
+            return at;
         };
         trg::KrOmega& o = kp.om[n];
-        o.A = table(0, n, &o.left);
+        slot[n].a = table(0, n, &o.left);
         if (n + 1 < N) {
-            o.F = table(n + 1, n + 2, &o.S1);
-            o.H = table(n + 2, N, &o.nH);
+            slot[n].f = table(n + 1, n + 2, &o.S1);
+            slot[n].h = table(n + 2, N, &o.nH);
         } else {
-            o.F = o.H = table(N, N, &o.nH);  // one row of ones
+            slot[n].f = slot[n].h = table(N, N, &o.nH);  // one row of ones
             o.S1 = 1;
         }
         require(o.S1 * o.nH < (int64_t(1) << 32), "sketch: Khatri-Rao row index beyond 32 bits");
@@ -790,14 +796,15 @@ KrPlan build_kr(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t se
     double* base = draws + total;
     kp.bufs.push_back(draws);
     trg::launch_omega(seed, 0, total, 1, draws, ctx->stream);
-    auto rebase = [&](const double* off_as_ptr) { return base + reinterpret_cast<intptr_t>(off_as_ptr); };
-    for (auto& t : tabs) t.out = const_cast<double*>(rebase(t.out));
+    for (size_t i = 0, at = 0; i < tabs.size(); ++i) {
+        tabs[i].out = base + at;
+        at += (size_t)(tabs[i].nrows * tabs[i].K);
+    }
     for (int n = 0; n < N; ++n)
-        if (K[n] != dims[n]) {  // (the first table sits at offset 0, i.e. "nullptr" until here)
-            trg::KrOmega& o = kp.om[n];
-            o.A = rebase(o.A);
-            o.F = rebase(o.F);
-            o.H = rebase(o.H);
+        if (K[n] != dims[n]) {
+            kp.om[n].A = base + slot[n].a;
+            kp.om[n].F = base + slot[n].f;
+            kp.om[n].H = base + slot[n].h;
         }
     trg::launch_kr_tables(draws, tabs.data(), (int)tabs.size(), ctx->stream);
     ctx->launches += 2;
