@@ -141,6 +141,8 @@ void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double*
 void launch_reduce_partials(const double* partial, int nblocks, int64_t n, double* out, cudaStream_t s);
 // the same sum (fixed order, a different one) spread over ~n / 16 CTAs with 16-byte loads
 void launch_reduce_wide(const double* partial, int nparts, int64_t n, double* out, cudaStream_t s);
+// zero n ints in a one-CTA kernel launched into the programmatic-launch chain
+void launch_zero_ints(int* p, int n, cudaStream_t s);
 
 // ---- thin QR with diag(R) >= 0 (K4): CholQR2 + Householder fallback, fp64.
 // Y is m x k column-major; Q (m x k) out. work >= m*k doubles + 2*k.

@@ -829,7 +829,13 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     if (!sk->ev1) CK(cudaEventCreate(&sk->ev1));
     CK(cudaEventRecord(sk->ev0, ctx->stream));
     sk->dflags = (int*)ctx->alloc(sizeof(int) * 3 * N);  // + N arrival tickets of the fused QR reduce
-    CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 3 * N, ctx->stream));
+    static const bool memset_flags = getenv("TRG_FLAGS_MEMSET") != nullptr;  // development switch
+    if (memset_flags) {
+        CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 3 * N, ctx->stream));
+    } else {
+        trg::launch_zero_ints(sk->dflags, 3 * N, ctx->stream);
+        ctx->launches += 1;
+    }
     sk->x = x;
     sk->seed = seed;
     if (allow_deferred && !kr_on && deferred_eligible(ctx, x, Kin, variant)) {

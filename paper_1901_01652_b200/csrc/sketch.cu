@@ -219,6 +219,13 @@ __global__ void __launch_bounds__(kRwThreads) k_reduce_wide(const double* __rest
     }
 }
 
+// zero n ints as a kernel in the programmatic-launch chain (a memset node between the previous
+// projection's last kernel and this one's first would cut the chain)
+__global__ void k_zero_ints(int* p, int n) {
+    griddep_wait();  // stream order with the previous kernel (which may still read the arena)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+
 __global__ void k_gauss_tables(GaussTables* t) {
     const int i = threadIdx.x;
     if (i < 128) {
@@ -352,6 +359,8 @@ void launch_reduce_partials(const double* partial, int nblocks, int64_t n, doubl
     const int blocks = (int)std::max<int64_t>(1, (n + 31) / 32);
     pdl_launch(k_reduce_partials, dim3(blocks), dim3(256), 0, s, partial, nblocks, n, out);
 }
+
+void launch_zero_ints(int* p, int n, cudaStream_t s) { pdl_launch(k_zero_ints, dim3(1), dim3(128), 0, s, p, n); }
 
 void launch_reduce_wide(const double* partial, int nparts, int64_t n, double* out, cudaStream_t s) {
     const int vec = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(partial) % 16 == 0);
