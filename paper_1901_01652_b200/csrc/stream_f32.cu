@@ -42,6 +42,9 @@ constexpr int kF32Cons = 8;
 #ifndef TRG_F32_GEN_LARGE
 #define TRG_F32_GEN_LARGE 4
 #endif
+#ifndef TRG_F32_GEN_MULTI
+#define TRG_F32_GEN_MULTI 8  // generator warps when K spans several TK blocks (C4's K_0 = 64): 1.24 -> 0.86 ms
+#endif
 constexpr int kF32Stages = 4;
 constexpr int kF32OB = 2;
 
@@ -510,6 +513,13 @@ int launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* partia
         cudaFuncSetAttribute(k_sketch_l1_f32<TKV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem); \
         k_sketch_l1_f32<TKV, G><<<grid, (kF32Cons + G + 1) * 32, p.smem, s>>>(map, a);                        \
     } while (0)
+    if (p.nkb > 1) {  // several k-blocks per tile: the Box-Muller generation is the bound
+        constexpr int G = TRG_F32_GEN_MULTI;
+        cudaFuncSetAttribute(k_sketch_l1_f32<16, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        k_sketch_l1_f32<16, G><<<grid, (kF32Cons + G + 1) * 32, p.smem, s>>>(map, a);
+        if (y) launch_reduce_partials(partial, gc, sp.dim * sp.K, y, s);
+        return gc;
+    }
     switch (p.TK) {
         case 4: TRG_F32(4); break;
         case 8: TRG_F32(8); break;
