@@ -76,6 +76,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // element (row d, column l < 16) of a 128B-swizzled stage, in doubles
 __device__ __forceinline__ int swz(int d, int l) { return d * 16 + ((((l >> 1) ^ (d & 7))) << 1) + (l & 1); }
 
+// unit u -> (slab r, left chunk lc) in 32-bit arithmetic (units < 2^31, slab2_ok): the 64-bit
+// division it replaces was a large part of the per-unit cost of the single producer thread
+__device__ __forceinline__ void unit_rc(int64_t u, int LC, int64_t& r, int& lc) {
+    if (LC == 1) {
+        r = u;
+        lc = 0;
+    } else {
+        const uint32_t q = (uint32_t)u / (uint32_t)LC;
+        r = q;
+        lc = (int)((uint32_t)u - q * (uint32_t)LC);
+    }
+}
+
 struct Slab2Args {
     int64_t left, dim, right;  // local view
     int LC;                    // ceil(left / 16) chunks per slab index
@@ -190,12 +203,13 @@ __global__ void __launch_bounds__((kSCons + 1) * 32, 1)
         if (lane == 0) {
             const uint64_t pol = policy_l2(a.pol);
             for (int64_t j = 0; j < nl; ++j) {
-                const int s = (int)(j % kStg);
-                mbar_wait(&empty[s], (uint32_t)((j / kStg) & 1) ^ 1u);
+                const int s = (int)j % kStg;
+                mbar_wait(&empty[s], (uint32_t)(((int)j / kStg) & 1) ^ 1u);
                 const int64_t u0 = blockIdx.x + j * gridDim.x;
                 const int64_t u = a.rev ? a.nunits - 1 - u0 : u0;
-                const int64_t r = u / a.LC;
-                const int lc = (int)(u - r * a.LC);
+                int64_t r;
+                int lc;
+                unit_rc(u, a.LC, r, lc);
                 unsigned char* st = base + s * sbytes;
 #ifdef TRG_DBG_NO_OMEGA_LOAD  // development: the test-matrix blocks not loaded (timing only)
                 mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128));
@@ -225,8 +239,8 @@ __global__ void __launch_bounds__((kSCons + 1) * 32, 1)
     for (int t = 0; t < 4; ++t) xoff[t] = 128 * mt0 + 16 * q + 2 * ((2 * t + (rl >> 1)) ^ q) + (rl & 1);
     const uint32_t sbase = smem_u32(base);
     for (int64_t j = pair; j < nl; j += 4) {
-        const int s = (int)(j % kStg);
-        mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
+        const int s = (int)j % kStg;
+        mbar_wait(&full[s], (uint32_t)(((int)j / kStg) & 1));
         const uint32_t xs = sbase + (uint32_t)(s * sbytes), os = xs + (uint32_t)xbytes;
         // groups past mt_extra run one tile fewer: compile-time counts, no predication
         if (MTW > 1 && my_mt == MTW - 1)
@@ -313,12 +327,13 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         if (lane == 0) {
             const uint64_t pol = policy_l2(a.pol);
             for (int64_t j = 0; j < nl; ++j) {
-                const int s = (int)(j % kStg);
-                mbar_wait(&empty[s], (uint32_t)((j / kStg) & 1) ^ 1u);
+                const int s = (int)j % kStg;
+                mbar_wait(&empty[s], (uint32_t)(((int)j / kStg) & 1) ^ 1u);
                 const int64_t u0 = blockIdx.x + j * gridDim.x;
                 const int64_t u = a.rev ? a.nunits - 1 - u0 : u0;
-                const int64_t r = u / a.LC;
-                const int lc = (int)(u - r * a.LC);
+                int64_t r;
+                int lc;
+                unit_rc(u, a.LC, r, lc);
                 mbar_arrive_expect_tx(&full[s], (uint32_t)(dim * 128));
                 tma_load_2d(base + s * sbytes, &tmap, kUnitL * lc, (int)(a.dim * r), &full[s], pol);
             }
@@ -350,8 +365,8 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
     }
     const uint32_t sbase = smem_u32(base);
     for (int64_t j = pair; j < nl; j += 4) {
-        const int s = (int)(j % kStg);
-        mbar_wait(&full[s], (uint32_t)((j / kStg) & 1));
+        const int s = (int)j % kStg;
+        mbar_wait(&full[s], (uint32_t)(((int)j / kStg) & 1));
         const uint32_t xs = sbase + (uint32_t)(s * sbytes);
         double acc[2][NT][2];  // [k-step parity][column tile][pair]
 #pragma unroll
@@ -370,8 +385,9 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
         mbar_arrive(&empty[s]);
         const int64_t u0 = blockIdx.x + j * gridDim.x;
         const int64_t u = a.rev ? a.nunits - 1 - u0 : u0;
-        const int64_t r = u / a.LC;
-        const int lc = (int)(u - r * a.LC);
+        int64_t r;
+        int lc;
+        unit_rc(u, a.LC, r, lc);
         // D fragment: (l = 8 mt + q, o = 8 jn + 2 rl + e) -> out(l_glob, o, r) at l + left (o + K r)
         const int64_t l = (int64_t)kUnitL * lc + 8 * mt + q;
         if (l < a.left) {
