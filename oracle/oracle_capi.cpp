@@ -162,6 +162,19 @@ int oracle_economy_q(std::int64_t rows, std::int64_t cols, const double* y, doub
     });
 }
 
+// Thin SVD stand-in for BDCSVD (solvers.hpp:398,431): singular values (min(rows, cols),
+// descending), U (rows x min) and V (cols x min), column-major. For the LAPACK cross-check.
+int oracle_svd(std::int64_t rows, std::int64_t cols, const double* a, double* s_out, double* u_out, double* v_out) {
+    return guard([&] {
+        Mat m(rows, cols);
+        std::memcpy(m.a.data(), a, sizeof(double) * m.a.size());
+        const SVD d = jacobi_svd(m);
+        std::memcpy(s_out, d.s.data(), sizeof(double) * d.s.size());
+        if (u_out) std::memcpy(u_out, d.U.a.data(), sizeof(double) * d.U.a.size());
+        if (v_out) std::memcpy(v_out, d.V.a.data(), sizeof(double) * d.V.a.size());
+    });
+}
+
 // Sequential (variant 0, sketch.hpp:62-89) or fused (variant 1)
 // projection. bases_out: concatenated I_n x K_n column-major (identity for
 // skipped modes); ys_out (optional): concatenated I_n x K_n sketches (zeros

@@ -534,6 +534,18 @@ inline SVD jacobi_svd(const Mat& a) {
         out.U = std::move(U);
         out.V = std::move(Vs);
     }
+    // Sign convention (ours; BDCSVD's signs are implementation-defined): the largest-magnitude
+    // entry of every left singular vector is positive. trsvd depends on these signs beyond its
+    // first split (tests/test_oracle_lapack.py), so product and oracle share this rule.
+    for (idx j = 0; j < out.U.c; ++j) {
+        idx arg = 0;
+        for (idx i = 1; i < out.U.r; ++i)
+            if (std::abs(out.U(i, j)) > std::abs(out.U(arg, j))) arg = i;
+        if (out.U(arg, j) < 0.0) {
+            for (idx i = 0; i < out.U.r; ++i) out.U(i, j) = -out.U(i, j);
+            for (idx i = 0; i < out.V.r; ++i) out.V(i, j) = -out.V(i, j);
+        }
+    }
     return out;
 }
 

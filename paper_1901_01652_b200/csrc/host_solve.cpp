@@ -507,6 +507,16 @@ void svd(const Mat& a, Mat& U, std::vector<double>& s, Mat& V) {
         U = std::move(Us);
         V = std::move(Vs);
     }
+    // sign convention shared with the oracle: largest-magnitude entry of each U column positive
+    for (idx j = 0; j < U.c; ++j) {
+        idx arg = 0;
+        for (idx i = 1; i < U.r; ++i)
+            if (std::abs(U(i, j)) > std::abs(U(arg, j))) arg = i;
+        if (U(arg, j) < 0.0) {
+            for (idx i = 0; i < U.r; ++i) U(i, j) = -U(i, j);
+            for (idx i = 0; i < V.r; ++i) V(i, j) = -V(i, j);
+        }
+    }
 }
 
 idx truncation_rank(const std::vector<double>& sv, double budget_sq, double* disc) {  // solvers.hpp:347-358

@@ -127,6 +127,18 @@ def economy_q(y):
     return out.reshape((y.shape[0], k), order="F")
 
 
+def svd(a):
+    """The oracle's thin SVD (one-sided Jacobi standing in for BDCSVD): (s, U, V)."""
+    a = np.asarray(a, dtype=np.float64)
+    af, ap = _f64(a)
+    k = min(a.shape)
+    s, sp = _out(k)
+    u, up = _out(a.shape[0] * k)
+    v, vp = _out(a.shape[1] * k)
+    _check(lib().oracle_svd(ctypes.c_int64(a.shape[0]), ctypes.c_int64(a.shape[1]), ap, sp, up, vp))
+    return s, u.reshape((a.shape[0], k), order="F"), v.reshape((a.shape[1], k), order="F")
+
+
 def sketch(x, K, seed, variant=0):
     """Returns (projected, bases, ys) — ys[n] is Y_n (zeros for skipped modes)."""
     x = np.asarray(x, dtype=np.float64)
