@@ -112,9 +112,8 @@ int trg_tensor_destroy(trg_tensor* t);
 /* ---- tensor random projection (sketch.hpp:62-89) ------------------------ */
 /* Enqueues the whole projection on the context stream and returns without
  * synchronising; the getters below synchronise. K has `order` entries,
- * 1 <= K_n <= I_n, K_n == I_n skips the mode (no draws). `x` must outlive the
- * sketch: with the opt-in deferred schedule (TRG_DEFERRED=1) the first getter
- * validates the run and may recompute it from x. */
+ * 1 <= K_n <= I_n, K_n == I_n skips the mode (no draws). The sketch does not
+ * keep a reference to `x`: once the enqueued work has run, x may be destroyed. */
 int trg_sketch_run(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t seed, int variant,
                    trg_sketch** out);
 int trg_sketch_projected(const trg_sketch* sk, double* out);     /* prod K_n, first-index-fastest */

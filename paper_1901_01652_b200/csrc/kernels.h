@@ -85,17 +85,6 @@ bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t 
 void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                            cudaStream_t s);
 
-// ---- fused mode-0 shrink + mode-1 sketch (K3), fp64, left == 1
-struct FusedPlan {
-    int64_t I0, I1, nfib, ldq, K0, K1;  // nfib = local mode-1 fibres = prod of local extents of modes >= 2
-    uint64_t seed, D1;
-    int64_t rows_glob1, col_off1;
-};
-bool fused_ttm_sketch_ok(int dtype, int64_t left, int64_t I0, int64_t K0, int64_t I1, int64_t K1);
-// out = P^(1), y1 = Y_1 (I1 x K1 col-major) via partial (grid x I1 x K1) and a fixed-order sum
-void launch_fused_ttm_sketch(const FusedPlan& p, const void* x, void* out, const double* q, double* partial,
-                             double* y1, int num_sms, cudaStream_t s);
-
 // ---- cp.async-gathered fp64 tensor-core kernels for modes with left > 1 (slab_f64.cu)
 bool slab_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
 void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
@@ -131,8 +120,6 @@ struct KrTable {
     int64_t off[kKrMaxFactors], rows[kKrMaxFactors];
 };
 void launch_kr_tables(const double* draws, const KrTable* tabs, int ntab, cudaStream_t s);
-// standard-layout test matrix (rows left*right, K columns) -> unit blocks
-void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s);
 int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
                         int num_sms, cudaStream_t s);
 void launch_slab2_ttm(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
@@ -157,8 +144,6 @@ bool qr_fused_ok(int64_t m, int k);
 // extra CTAs of the same launch (num_sms of them minus the reducing ones) while it is latency-bound.
 int launch_qr_fused(const double* part, int nparts, int64_t m, int k, double* y, double* q, double* work, int* flag,
                     int* ticket, cudaStream_t s, const OmegaUnitsJob* job = nullptr, int num_sms = 0);
-// Rinv = (upper(Q^T Y))^-1, k x k col-major, so that Q = Y Rinv; *bad set if R is near-singular
-void launch_rinv(const double* q, const double* y, int64_t m, int k, double* rinv, int* bad, cudaStream_t s);
 
 // ---- per-device tables of the table-driven Box-Muller (common.cuh), built on first use
 const GaussTables* gauss_tables(cudaStream_t s);

@@ -136,6 +136,7 @@ struct trg_ctx {
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // test-matrix generation for later modes, overlapped with QR / shrink
+    cudaMemPool_t pool = nullptr;  // private stream-ordered pool (release threshold: keep)
     ncclComm_t comm = nullptr;
     bool profiling = false;
     int64_t launches = 0;
@@ -187,7 +188,7 @@ struct trg_ctx {
     void* alloc(size_t bytes) {
         void* p = nullptr;
         if (bytes == 0) bytes = 8;
-        CK(cudaMallocAsync(&p, bytes, stream));
+        CK(cudaMallocFromPoolAsync(&p, bytes, pool, stream));
         return p;
     }
     void dfree(void* p) {
@@ -205,7 +206,7 @@ struct trg_ctx {
         if (scr_need > scr_cap) {
             if (scr_base) cudaFreeAsync(scr_base, stream);
             scr_cap = scr_need + scr_need / 4;
-            CK(cudaMallocAsync((void**)&scr_base, scr_cap, stream));
+            CK(cudaMallocFromPoolAsync((void**)&scr_base, scr_cap, pool, stream));
         }
         scr_off = 0;
         scr_active = true;
@@ -269,15 +270,11 @@ struct trg_sketch {
     std::vector<int64_t> dims, K;
     std::vector<double*> dQ;  // device Q_n (nullptr for skipped modes)
     std::vector<double*> dY;  // device Y_n full rows
-    int* dflags = nullptr;    // N QR-path flags, (deferred) N near-singular-R flags, N QR-reduce tickets
+    int* dflags = nullptr;    // N QR-path flags, N (unused), N QR-reduce tickets
     void* dP = nullptr;       // device P (dtype), full prod K
     bool P_is_view = false;   // P aliases x (no mode projected, unsharded)
     int64_t P_elems = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // deferred projection (run_sketch_deferred): validated lazily when results are read
-    const trg_tensor* x = nullptr;
-    uint64_t seed = 0;
-    bool deferred = false, checked = true;
     void release() {
         for (double*& p : dQ) ctx->dfree(p), p = nullptr;
         for (double*& p : dY) ctx->dfree(p), p = nullptr;
@@ -557,158 +554,6 @@ void schedule_pre_omega(trg_ctx* ctx, const trg_tensor* x, int later_dt, const s
     CK(cudaEventDestroy(go));
 }
 
-// ------------------------------------------------------------------ deferred projection
-// Q_n = Y_n Rinv_n for any QR with invertible R (here Rinv = upper(Q_n^T Y_n)^-1), so
-//   P^(n+1) = P^(n) x_n Q_n^T = (P^(n) x_n Y_n^T) x_n Rinv_n^T,
-// and mode products on different modes commute. The shrink of mode n can therefore start as
-// soon as Y_n is reduced, with Y_n in place of Q_n, while the QR of Y_n (a one-SM,
-// latency-bound kernel) runs on the side stream; the deferred factors are folded into
-//   * the next modes' test matrices: with Ptilde = X x_m Y_m^T (m < n), the mode-n sketch
-//     P^(n)_(n) Omega_n equals Ptilde_(n) Omegatilde_n, Omegatilde_n = Omega_n x_0 Rinv_0
-//     x_1 Rinv_1 ... (a small transform of the L2-resident test matrix, side stream), and
-//   * the final P = Ptilde x_0 Rinv_0^T x_1 ... (tiny).
-// Mathematically this is the reference's sequential projection (sketch.hpp:62-89) with the
-// same Omega draws; only the association order of the products changes. If any QR takes the
-// Householder path or R is near-singular, the result is recomputed eagerly when it is read.
-// Opt-in (TRG_DEFERRED=1): measured slower on C2 so far (profiles/README.md): the persistent
-// one-CTA-per-SM streaming kernels leave no room for the side stream's QR / transform
-// kernels, so the side pipeline serialises behind them instead of overlapping.
-bool deferred_eligible(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, int variant) {
-    static const bool on = getenv("TRG_DEFERRED") != nullptr;
-    if (!on || ctx->world != 1 || variant != TRG_SEQUENTIAL) return false;
-    const int N = (int)x->dims.size();
-    std::vector<int64_t> shape = x->local_shape();
-    int cdt = x->dtype;
-    bool first = true;
-    for (int n = 0; n < N; ++n) {
-        if (K[n] == x->dims[n]) continue;
-        const int64_t left = prod(shape, 0, n), dim = shape[n], right = prod(shape, n + 1);
-        if (first) {
-            if (trg::stream_ttm_f32_ok(cdt, left, dim, K[n], right)) cdt = F64;
-            first = false;
-        } else if (!(left > 1 && trg::slab2_ok(cdt, left, dim, K[n], right))) {
-            return false;  // later modes must take their test matrix from memory (slab kernels)
-        }
-        shape[n] = K[n];
-    }
-    return !first;
-}
-
-void run_sketch_deferred(trg_ctx* ctx, const trg_tensor* x, uint64_t seed, trg_sketch* sk) {
-    const int N = (int)x->dims.size();
-    const std::vector<int64_t>& K = sk->K;
-    const std::vector<ModeOffsets> offs = sketch_offsets(x->dims, K.data(), x->lo, TRG_SEQUENTIAL);
-    std::vector<int> proj;
-    for (int n = 0; n < N; ++n)
-        if (K[n] != x->dims[n]) proj.push_back(n);
-    std::vector<int64_t> shape = x->local_shape();
-    int cdt = x->dtype;
-    const void* cur = x->d;
-    void* owned = nullptr;
-    std::vector<double*> rinv(N, nullptr);
-    std::vector<cudaEvent_t> ev_y(N, nullptr), ev_r(N, nullptr);
-    std::vector<PreOmega> pre(N);
-    auto mk_event = [&]() {
-        cudaEvent_t e;
-        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        return e;
-    };
-    auto side_alloc = [&](size_t bytes) {
-        void* p = nullptr;
-        CK(cudaMallocAsync(&p, bytes ? bytes : 8, ctx->side));
-        return p;
-    };
-    for (size_t idx = 0; idx < proj.size(); ++idx) {
-        const int n = proj[idx];
-        const int64_t In = x->dims[n], Kn = K[n];
-        sk->dY[n] = (double*)ctx->alloc(sizeof(double) * In * Kn);
-        sk->dQ[n] = (double*)ctx->alloc(sizeof(double) * In * Kn);
-        rinv[n] = (double*)ctx->alloc(sizeof(double) * Kn * Kn);
-        sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], idx ? &pre[n] : nullptr);
-        ev_y[n] = mk_event();
-        CK(cudaEventRecord(ev_y[n], ctx->stream));
-        // ---- side stream: QR of Y_n, Rinv_n, and the next mode's transformed test matrix
-        CK(cudaStreamWaitEvent(ctx->side, ev_y[n], 0));
-        double* work = (double*)side_alloc(sizeof(double) * In * Kn);
-        trg::launch_qr(sk->dY[n], In, (int)Kn, sk->dQ[n], work, sk->dflags + n, ctx->side);
-        CK(cudaFreeAsync(work, ctx->side));
-        trg::launch_rinv(sk->dQ[n], sk->dY[n], In, (int)Kn, rinv[n], sk->dflags + N + n, ctx->side);
-        ctx->launches += 2;
-        ev_r[n] = mk_event();
-        CK(cudaEventRecord(ev_r[n], ctx->side));
-        if (idx + 1 < proj.size()) {
-            const int m = proj[idx + 1];
-            std::vector<int64_t> sm = shape;  // the working shape at mode m
-            sm[n] = Kn;
-            const int64_t left = prod(sm, 0, m), right = prod(sm, m + 1), Km = K[m];
-            const int64_t rows = left * right;
-            double* om = (double*)side_alloc(sizeof(double) * rows * Km);
-            trg::launch_omega(seed, offs[m].D, offs[m].rows_glob, Km, om, ctx->side);  // rows_glob == rows here
-            // Omegatilde = Omega x_j Rinv_j for every earlier projected mode j, on the view
-            // (sm[0], ..., sm[m-1], right * K_m)
-            for (size_t jj = 0; jj <= idx; ++jj) {
-                const int j = proj[jj];
-                trg::TTMPlan tp{};
-                tp.dtype = F64;
-                tp.left = prod(sm, 0, j);
-                tp.dim = K[j];
-                tp.right = prod(sm, j + 1, m) * right * Km;
-                tp.odim = K[j];
-                tp.m_so = 1;  // M(o, d) = Rinv_j[o + K_j d]
-                tp.m_sd = K[j];
-                trg::plan_ttm(tp, ctx->num_sms);
-                double* o2 = (double*)side_alloc(sizeof(double) * rows * Km);
-                trg::launch_ttm(tp, om, o2, rinv[j], ctx->side);
-                CK(cudaFreeAsync(om, ctx->side));
-                om = o2;
-            }
-            const int NT = Km <= 8 ? 1 : 2;
-            pre[m].buf = (double*)side_alloc(sizeof(double) * trg::slab2_units(left, right) * 4 * NT * 32);
-            trg::launch_pack_units(om, left, right, (int)Km, pre[m].buf, ctx->side);
-            CK(cudaFreeAsync(om, ctx->side));
-            ctx->launches += 3 + (int64_t)idx + 1;
-            pre[m].ready = mk_event();
-            CK(cudaEventRecord(pre[m].ready, ctx->side));
-        }
-        // ---- main stream: shrink with Y_n in place of Q_n
-        int odt = cdt;
-        void* out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dY[n], &odt);
-        if (owned) ctx->dfree(owned);
-        owned = out;
-        cur = out;
-        cdt = odt;
-        shape[n] = Kn;
-    }
-    // ---- fold the deferred factors into P: P = Ptilde x_j Rinv_j^T
-    for (int n : proj) {
-        CK(cudaStreamWaitEvent(ctx->stream, ev_r[n], 0));
-        trg::TTMPlan tp{};
-        tp.dtype = cdt;
-        tp.left = prod(shape, 0, n);
-        tp.dim = K[n];
-        tp.right = prod(shape, n + 1);
-        tp.odim = K[n];
-        tp.m_so = K[n];  // M(o, d) = Rinv_n^T(o, d) = Rinv_n[d + K_n o]
-        tp.m_sd = 1;
-        trg::plan_ttm(tp, ctx->num_sms);
-        void* o2 = ctx->alloc(trg::dtype_size(cdt) * (size_t)prod(shape));
-        ctx->launch("rinv_fold", [&] { trg::launch_ttm(tp, cur, o2, rinv[n], ctx->stream); });
-        ctx->dfree(owned);
-        owned = o2;
-        cur = o2;
-    }
-    for (int n : proj) {
-        ctx->dfree(rinv[n]);
-        cudaEventDestroy(ev_y[n]);
-        cudaEventDestroy(ev_r[n]);
-        if (pre[n].ready) cudaEventDestroy(pre[n].ready);
-    }
-    sk->P_elems = prod(shape);
-    sk->dtype = cdt;
-    sk->dP = owned;
-    sk->P_is_view = false;
-}
-
 // ------------------------------------------------------------------ Khatri-Rao test matrices (f4)
 // Omega_n(c, k) = prod_{m != n} F_{n,m}(i_m, k) for unfolding column c = sum_{m != n} i_m stride_m
 // (first index fastest), F_{n,m} an S_m x K_n block of the stream `seed` (trg.h
@@ -811,8 +656,7 @@ KrPlan build_kr(trg_ctx* ctx, const trg_tensor* x, const int64_t* K, uint64_t se
     return kp;
 }
 
-void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk,
-                bool allow_deferred = true) {
+void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t seed, int variant, trg_sketch* sk) {
     const int N = (int)x->dims.size();
     validate_K(x, Kin);
     const bool kr_on = (variant & TRG_OMEGA_KHATRI_RAO) != 0;
@@ -836,17 +680,6 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
         trg::launch_zero_ints(sk->dflags, 3 * N, ctx->stream);
         ctx->launches += 1;
     }
-    sk->x = x;
-    sk->seed = seed;
-    if (allow_deferred && !kr_on && deferred_eligible(ctx, x, Kin, variant)) {
-        sk->deferred = true;
-        sk->checked = false;
-        run_sketch_deferred(ctx, x, seed, sk);
-        CK(cudaEventRecord(sk->ev1, ctx->stream));
-        return;
-    }
-    sk->deferred = false;
-    sk->checked = true;
     const KrPlan krp = kr_on ? build_kr(ctx, x, Kin, seed, variant) : KrPlan{};
     auto krn = [&](int n) { return kr_on ? &krp.om[n] : nullptr; };
     ctx->scr_begin();
@@ -897,12 +730,10 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
 
     bool pre_started = false;
     if (variant == TRG_SEQUENTIAL) {
-        std::vector<bool> y_ready(N, false);
         for (int n = 0; n < N; ++n) {
             const int64_t Kn = sk->K[n];
             if (Kn == x->dims[n]) continue;  // identity basis, no draws (sketch.hpp:76-79)
-            if (!y_ready[n])
-                sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n], krn(n));
+            sketch_mode(ctx, x, cdt, cur, shape, n, Kn, seed, offs[n], sk->dY[n], &pre[n], &yparts[n], krn(n));
             static const bool side_omega = getenv("TRG_SIDE_OMEGA") != nullptr;
             if (!pre_started && yparts[n].partial && !side_omega) {
                 // ticketed QR launches: their CTAs past the reduce generate the later test
@@ -925,45 +756,13 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                                    kr_on ? &krp.om : nullptr);
             }
             const bool join_after_shrink = n == first_proj;
-            void* out = nullptr;
             const bool escape = n == last_proj;  // the last shrink writes P itself
-            // K3: fuse this shrink with the next mode's sketch while P^(1) tiles are on chip
-            // off by default: the separate shrink + TMA slab sketch measure faster (profiles/)
-            static const bool fuse = getenv("TRG_FUSE") != nullptr;
-            if (fuse && !kr_on && n == 0 && N >= 3 && sk->K[1] != x->dims[1] &&
-                trg::fused_ttm_sketch_ok(cdt, 1, shape[0], Kn, shape[1], sk->K[1])) {
-                trg::FusedPlan fp{};
-                fp.I0 = shape[0];
-                fp.I1 = shape[1];
-                fp.nfib = prod(shape, 2);
-                fp.ldq = x->dims[0];
-                fp.K0 = Kn;
-                fp.K1 = sk->K[1];
-                fp.seed = seed;
-                fp.D1 = offs[1].D;
-                fp.rows_glob1 = offs[1].rows_glob;
-                fp.col_off1 = offs[1].col_off;
-                out = ctx->tmp(trg::dtype_size(cdt) * (size_t)(Kn * prod(shape, 1)));
-                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(fp.nfib, ctx->num_sms));
-                double* partial = (double*)ctx->tmp(sizeof(double) * grid * fp.I1 * fp.K1);
-                ctx->launch("ttm_m0+sketch_m1", [&] {
-                    trg::launch_fused_ttm_sketch(fp, cur, out, sk->dQ[0], partial, sk->dY[1], ctx->num_sms,
-                                                 ctx->stream);
-                }, 2);
-                ctx->tmp_free(partial);
-                ctx->allreduce(sk->dY[1], (size_t)(x->dims[1] * sk->K[1]), F64);
-                y_ready[1] = true;
-                release_owned();
-                owned = out;
-                owned_arena = true;
-            } else {
-                int odt = cdt;
-                out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt, escape, /*chain=*/true);
-                cdt = odt;
-                release_owned();
-                owned = out;
-                owned_arena = !escape;
-            }
+            int odt = cdt;
+            void* out = shrink_mode(ctx, x, cdt, cur, shape, n, Kn, sk->dQ[n], &odt, escape, /*chain=*/true);
+            cdt = odt;
+            release_owned();
+            owned = out;
+            owned_arena = !escape;
             if (join_after_shrink) {
                 // join the side stream once, here, rather than before every later sketch: each
                 // cross-stream wait cuts a programmatic-dependent-launch edge of the chain
@@ -1043,30 +842,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     CK(cudaEventRecord(sk->ev1, ctx->stream));
 }
 
-// Deferred projections are checked when first read: a Householder-path QR or a near-singular
-// R invalidates the Y-for-Q substitution, and the projection is then recomputed eagerly.
-void validate(const trg_sketch* csk) {
-    trg_sketch* sk = const_cast<trg_sketch*>(csk);
-    if (!sk->deferred || sk->checked) return;
-    const int N = (int)sk->dims.size();
-    std::vector<int> f(2 * N);
-    CK(cudaMemcpyAsync(f.data(), sk->dflags, sizeof(int) * 2 * N, cudaMemcpyDeviceToHost, sk->ctx->stream));
-    CK(cudaStreamSynchronize(sk->ctx->stream));
-    sk->checked = true;
-    bool bad = false;
-    for (int v : f) bad = bad || v != 0;
-    if (!bad) return;
-    trg_ctx* ctx = sk->ctx;
-    const trg_tensor* x = sk->x;
-    const std::vector<int64_t> K = sk->K;
-    const uint64_t seed = sk->seed;
-    sk->release();
-    run_sketch(ctx, x, K.data(), seed, TRG_SEQUENTIAL, sk, /*allow_deferred=*/false);
-    CK(cudaStreamSynchronize(ctx->stream));
-}
-
 void download_P(const trg_sketch* sk, std::vector<double>& out) {
-    validate(sk);
     trg_ctx* ctx = sk->ctx;
     out.resize((size_t)sk->P_elems);
     if (sk->dtype == F64) {
@@ -1081,7 +857,6 @@ void download_P(const trg_sketch* sk, std::vector<double>& out) {
 }
 
 void download_basis(const trg_sketch* sk, int n, double* out) {
-    validate(sk);
     const int64_t In = sk->dims[n], Kn = sk->K[n];
     if (!sk->dQ[n]) {
         for (int64_t j = 0; j < Kn; ++j)
@@ -1310,7 +1085,7 @@ trg_tensor* tensor_new(trg_ctx* ctx, int dtype, int order, const int64_t* dims) 
     CK(cudaSetDevice(ctx->device));
     // from the context's stream-ordered pool (release threshold: keep), so repeated
     // create/destroy (trg_decompose_host per call) costs no driver allocation or implicit sync
-    CK(cudaMallocAsync(&t->d, trg::dtype_size(dtype) * (size_t)t->local_elems, ctx->stream));
+    CK(cudaMallocFromPoolAsync(&t->d, trg::dtype_size(dtype) * (size_t)t->local_elems, ctx->pool, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // usable from any stream on return
     return t.release();
 }
@@ -1370,10 +1145,15 @@ static void ctx_init(trg_ctx* c, int device) {
                                        std::to_string(major));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-    cudaMemPool_t pool;
-    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    // a private pool, so keeping freed memory (no driver call or implicit sync per projection) does
+    // not change the process-global default pool other libraries allocate from
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    CK(cudaMemPoolCreate(&c->pool, &props));
     uint64_t thr = UINT64_MAX;
-    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
 int trg_ctx_create(int device, trg_ctx** out) {
@@ -1422,9 +1202,12 @@ int trg_ctx_destroy(trg_ctx* ctx) {
         for (auto e : ctx->event_pool) cudaEventDestroy(e);
         if (ctx->comm) nccl().commDestroy(ctx->comm);
         cudaStreamSynchronize(ctx->side);
-        if (ctx->scr_base) cudaFree(ctx->scr_base);
+        if (ctx->scr_base) cudaFreeAsync(ctx->scr_base, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->side);
         cudaStreamDestroy(ctx->stream);
+        // outstanding allocations (tensors not destroyed yet) keep the pool alive until freed
+        if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
         delete ctx;
     });
 }
@@ -1597,8 +1380,7 @@ int trg_sketch_basis(const trg_sketch* sk, int mode, double* out) {
 
 int trg_sketch_y(const trg_sketch* sk, int mode, double* out) {
     return guard([&] {
-        validate(sk);
-        if (mode < 0 || mode >= (int)sk->dims.size())
+            if (mode < 0 || mode >= (int)sk->dims.size())
             throw std::out_of_range("DenseTensor: mode " + std::to_string(mode) + " out of range");
         const int64_t n = sk->dims[mode] * sk->K[mode];
         if (!sk->dY[mode]) {
@@ -1612,8 +1394,7 @@ int trg_sketch_y(const trg_sketch* sk, int mode, double* out) {
 
 int trg_sketch_qr_path(const trg_sketch* sk, int mode, int* hh) {
     return guard([&] {
-        validate(sk);
-        if (mode < 0 || mode >= (int)sk->dims.size()) throw std::out_of_range("mode out of range");
+            if (mode < 0 || mode >= (int)sk->dims.size()) throw std::out_of_range("mode out of range");
         int v = 0;
         CK(cudaMemcpyAsync(&v, sk->dflags + mode, sizeof(int), cudaMemcpyDeviceToHost, sk->ctx->stream));
         CK(cudaStreamSynchronize(sk->ctx->stream));
@@ -1737,7 +1518,6 @@ static trg_tensor* lift_back_device(trg_ctx* ctx, int dtype, const std::vector<i
 
 int trg_sketch_lift_back(const trg_sketch* csk, trg_tensor** out) {
     return guard([&] {
-        validate(csk);
         const trg_sketch* sk = csk;
         std::vector<const double*> q(sk->dims.size());
         for (size_t n = 0; n < q.size(); ++n) q[n] = sk->K[n] == sk->dims[n] ? nullptr : sk->dQ[n];

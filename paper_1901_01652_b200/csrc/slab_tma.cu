@@ -73,8 +73,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// element (row d, column l < 16) of a 128B-swizzled stage, in doubles
-__device__ __forceinline__ int swz(int d, int l) { return d * 16 + ((((l >> 1) ^ (d & 7))) << 1) + (l & 1); }
 
 // unit u -> (slab r, left chunk lc) in 32-bit arithmetic (units < 2^31, slab2_ok): the 64-bit
 // division it replaces was a large part of the per-unit cost of the single producer thread
@@ -404,23 +402,6 @@ __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
 }
 
 
-// Re-block a test matrix given in the standard layout (rows c = l + left r, K columns,
-// column-major) into the unit blocks consumed by k_slab2_sketch_f64 (the deferred projection
-// transforms Omega_n in the standard layout first).
-__global__ void k_pack_units(const double* __restrict__ om, int64_t rows, int64_t left, int LC, int64_t nunits, int K,
-                             int NT, double* out) {
-    const int64_t per = 4 * NT * 32;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nunits * per; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = e / per;
-        const int w = (int)(e - u * per);
-        const int lane = w & 31, jn = (w >> 5) % NT, t = (w >> 5) / NT;
-        const int64_t r = u / LC;
-        const int lc = (int)(u - r * LC);
-        const int64_t l = (int64_t)kUnitL * lc + 4 * t + (lane & 3);
-        const int k = 8 * jn + (lane >> 2);
-        out[e] = (l < left && k < K) ? om[(l + left * r) + rows * k] : 0.0;
-    }
-}
 
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -472,6 +453,7 @@ void set_smem(KernelT k, size_t smem) {
 bool slab2_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right) {
     if (dtype != F64 || left < 2 || (left & 1) || dim > 128 || K > 16 || !encode_fn()) return false;
     if (dim * right >= (int64_t(1) << 31) || left >= (int64_t(1) << 31)) return false;  // TMA coordinates are int32
+    if (slab2_units(left, right) >= (int64_t(1) << 31)) return false;  // 32-bit unit index math (unit_rc)
     return stages_for(sketch_stage(dim, 2)) >= 4 && stages_for(ttm_stage(dim)) >= 4;
 }
 
@@ -520,14 +502,6 @@ void launch_omega_units(int64_t left, int64_t right, int K, uint64_t seed, uint6
     k_omega_units<<<blocks, threads, 0, s>>>(j);
 }
 
-void launch_pack_units(const double* om, int64_t left, int64_t right, int K, double* out, cudaStream_t s) {
-    const int LC = (int)((left + kUnitL - 1) / kUnitL);
-    const int64_t nunits = right * LC;
-    const int NT = K <= 8 ? 1 : 2;
-    const int64_t n = nunits * 4 * NT * 32;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
-    k_pack_units<<<blocks, 256, 0, s>>>(om, left * right, left, LC, nunits, K, NT, out);
-}
 
 int launch_slab2_sketch(const SketchPlan& p, const void* x, const double* omega_units, double* partial, double* y,
                          int num_sms, cudaStream_t s) {

@@ -103,11 +103,7 @@ __device__ __forceinline__ void sk_consume(double (&acc)[MTW][NT][2], const doub
         for (int mt = 0; mt < NMT; ++mt)
 #pragma unroll
             for (int jn = 0; jn < NT; ++jn) {
-#ifdef TRG_SK_NOMMA  // measurement only: the tensor work removed
-                acc[mt][jn][0] += av[mt] * bv[jn];
-#else
                 dmma884(acc[mt][jn][0], acc[mt][jn][1], av[mt], bv[jn]);
-#endif
             }
     }
 }
@@ -302,9 +298,6 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                 for (int u = 0; u < kIlp; ++u)
 #pragma unroll
                     for (int i = 0; i < kIpt; ++i) {
-#ifdef TRG_SK_NOGEN  // measurement only: the generator's cost removed
-                        z[u][i][0] = z[u][i][1] = (double)(st[i] & 7u) * 0.25;
-#else
                         if constexpr (kr) {  // products of the factor entries (L1-resident): no draws
                             const int64_t cl = (blockIdx.x + (int64_t)(j + u * R) * gridDim.x) * CT + c0[i];
                             const uint32_t cg = (uint32_t)(a.col_off + cl);
@@ -314,7 +307,6 @@ __global__ void __launch_bounds__((kSkCons + kRng + 1) * 32, 1) k_sketch_l1_f64(
                             gauss_pair_state(u == 0 ? st[i] : st[i] + (uint64_t)u * incR, *tabs, z[u][i][0],
                                              z[u][i][1]);
                         }
-#endif
                     }
 #pragma unroll
                 for (int i = 0; i < kIpt; ++i) st[i] += incG;
@@ -583,219 +575,6 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1) k_ttm_l1_f64(TtmArgs a) {
 }
 
 
-// ---------------------------------------------------------------- fused shrink + next sketch
-// K3: P^(1) = X x_0 Q_0^T and, while each P^(1) tile is still in
-// registers, Y_1 += P^(1)_(1) Omega_1, so P^(1) is written once and never read
-// back for the mode-1 sketch (sketch.hpp:85 followed by :80-83 of mode 1).
-// A work item is one mode-1 fibre f = (i_2, ...) of P^(1): rows m = i_1 + I_1 f
-// of X_(0)^T (I_1 <= 128 rows, processed as H <= 2 row blocks of 64). For that
-// fibre P^(1)_(1) contributes the columns c = o + K_0 f, so
-//   Y_1(i_1, k) += sum_o P1(i_1, o) Omega_1(o + K_0 f, k)
-// is a (rows x K_0)(K_0 x K_1) DMMA whose A fragments come from the shrink's
-// accumulators by quad shuffles and whose B fragments (the K_0 x K_1 block of
-// the reference test matrix) are regenerated per fibre by two generator warps.
-constexpr int kFCons = 4;  // consumer warps: 16 rows each, 64 rows per block
-constexpr int kFGen = 2;   // Omega_1 generator warps
-
-struct FusedArgs {
-    const double* x;     // X, read as rows of I_0
-    double* out;         // P^(1), rows of K_0
-    const double* q;     // Q_0 (ldq x K0 col-major)
-    double* partial;     // per-CTA Y_1 partial (I_1 x K_1 col-major)
-    const GaussTables* gt;
-    int64_t I0, I1, nfib, ldq;
-    int K0, K1, Tk, H, ks;  // ks = ceil(K0 / 4) k-steps of the sketch product
-    uint64_t seed, D1;
-    int64_t rows_glob1, col_off1;
-};
-
-template <int NT0, int NT1>
-__global__ void __launch_bounds__((kFCons + kFGen + 1) * 32, 1) k_ttm_sketch_l1_f64(FusedArgs a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int64_t I0 = a.I0;
-    const int stage_elems = (int)(64 * I0) + kPad;
-    double* stages = reinterpret_cast<double*>(smem_raw);
-    double* Bf = stages + kStages * stage_elems;  // Q_0 in B-fragment order
-    const int bf_elems = a.Tk * NT0 * 32;
-    double* Ob = Bf + bf_elems;  // 2 Omega_1 blocks in B-fragment order
-    const int ob_elems = a.ks * NT1 * 32;
-    GaussTables* tabs = reinterpret_cast<GaussTables*>(Ob + 2 * ob_elems);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tabs + 1);
-    uint64_t* full_x = bars;
-    uint64_t* empty_x = bars + kStages;
-    uint64_t* full_o = bars + 2 * kStages;
-    uint64_t* empty_o = bars + 2 * kStages + 2;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nf = (int)((a.nfib - blockIdx.x + gridDim.x - 1) / gridDim.x);  // fibres of this CTA
-    const int nitems = nf * a.H;
-
-    for (int i = tid; i < kStages * stage_elems; i += blockDim.x) stages[i] = 0.0;
-    for (int i = tid; i < 2 * ob_elems; i += blockDim.x) Ob[i] = 0.0;
-    for (int i = tid; i < bf_elems; i += blockDim.x) {
-        const int t = i / (NT0 * 32);
-        const int jn = (i >> 5) % NT0;
-        const int ln = i & 31;
-        const int64_t d = 4 * t + (ln & 3);
-        const int o = 8 * jn + (ln >> 2);
-        Bf[i] = (d < I0 && o < a.K0) ? a.q[d + a.ldq * o] : 0.0;
-    }
-    gauss_tables_to_smem(*tabs, a.gt);
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full_x[s], 1);
-            mbar_init(&empty_x[s], kFCons * 32);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&full_o[b], kFGen * 32);
-            mbar_init(&empty_o[b], kFCons * 32);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == kFCons + kFGen) {
-        // ---------------- producer: one TMA bulk copy per 64-row block of a fibre
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            for (int j = 0; j < nitems; ++j) {
-                const int s = j % kStages;
-                mbar_wait(&empty_x[s], ((j / kStages) & 1) ^ 1);
-                const int64_t f = blockIdx.x + (int64_t)(j / a.H) * gridDim.x;
-                const int h = j % a.H;
-                const int64_t m0 = f * a.I1 + 64 * h;
-                const int64_t nrow = imin64(64, a.I1 - 64 * h);
-                const uint32_t bytes = (uint32_t)(nrow * I0 * 8);
-                mbar_arrive_expect_tx(&full_x[s], bytes);
-                bulk_g2s(stages + s * stage_elems, a.x + m0 * I0, bytes, &full_x[s], pol);
-            }
-        }
-        return;
-    }
-    if (warp >= kFCons) {
-        // ---------------- generators: Omega_1 rows o + K_0 f (o < K_0), all K_1 columns
-        const int gt = tid - kFCons * 32;
-        const int npk = a.K0 / 2 + 1;  // pairs covering K_0 consecutive draws
-        for (int i = 0; i < nf; ++i) {
-            const int b = i & 1;
-            mbar_wait(&empty_o[b], ((i >> 1) & 1) ^ 1);
-            const int64_t f = blockIdx.x + (int64_t)i * gridDim.x;
-            double* O = Ob + b * ob_elems;
-            for (int it = gt; it < a.K1 * npk; it += kFGen * 32) {
-                const int k = it / npk, jj = it - k * npk;
-                const uint64_t s0 = a.D1 + (uint64_t)(a.col_off1 + a.K0 * f) + (uint64_t)a.rows_glob1 * (uint64_t)k;
-                const uint64_t p = (s0 >> 1) + (uint64_t)jj;
-                if (p > ((s0 + (uint64_t)a.K0 - 1ull) >> 1)) continue;
-                double z0, z1;
-                gauss_pair_tab(a.seed, p, *tabs, z0, z1);
-                const int64_t o = (int64_t)(2ull * p - s0);
-                if (o >= 0 && o < a.K0) O[(((o >> 2) * NT1 + (k >> 3)) << 5) + (o & 3) + ((k & 7) << 2)] = z0;
-                if (o + 1 >= 0 && o + 1 < a.K0)
-                    O[((((o + 1) >> 2) * NT1 + (k >> 3)) << 5) + ((o + 1) & 3) + ((k & 7) << 2)] = z1;
-            }
-            mbar_arrive(&full_o[b]);
-        }
-        return;
-    }
-    // ---------------- consumers: warp w owns rows 16w..16w+15 of every 64-row block
-    const int q = lane >> 2, r = lane & 3;
-    double yacc[2][2][NT1][2];  // [row block h][row tile][column tile][pair]
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int jn = 0; jn < NT1; ++jn) yacc[h][mt][jn][0] = yacc[h][mt][jn][1] = 0.0;
-    for (int j = 0; j < nitems; ++j) {
-        const int s = j % kStages;
-        const int i = j / a.H, h = j % a.H;
-        mbar_wait(&full_x[s], (j / kStages) & 1);
-        const double* x0 = stages + s * stage_elems + (16 * warp + q) * I0 + r;
-        const double* x1 = x0 + 8 * I0;
-        double acc[2][NT0][2];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int jn = 0; jn < NT0; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
-#pragma unroll 4
-        for (int t = 0; t < a.Tk; ++t) {
-            double bv[NT0];
-#pragma unroll
-            for (int jn = 0; jn < NT0; ++jn) bv[jn] = Bf[((t * NT0 + jn) << 5) + lane];
-            const double a0 = x0[4 * t], a1 = x1[4 * t];
-#pragma unroll
-            for (int jn = 0; jn < NT0; ++jn) {
-                dmma884(acc[0][jn][0], acc[0][jn][1], a0, bv[jn]);
-                dmma884(acc[1][jn][0], acc[1][jn][1], a1, bv[jn]);
-            }
-        }
-        mbar_arrive(&empty_x[s]);
-        const int64_t f = blockIdx.x + (int64_t)i * gridDim.x;
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            const int row = 64 * h + 16 * warp + 8 * mt + q;  // i_1 of this lane's accumulator row
-            if (row < a.I1) {
-                double* dst = a.out + (f * a.I1 + row) * a.K0;
-#pragma unroll
-                for (int jn = 0; jn < NT0; ++jn) {
-                    const int o = 8 * jn + 2 * r;
-                    if (o + 1 < a.K0 && !(a.K0 & 1)) {
-                        *reinterpret_cast<double2*>(dst + o) = make_double2(acc[mt][jn][0], acc[mt][jn][1]);
-                    } else {
-                        if (o < a.K0) dst[o] = acc[mt][jn][0];
-                        if (o + 1 < a.K0) dst[o + 1] = acc[mt][jn][1];
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int jn = 0; jn < NT0; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
-            }
-        }
-        // sketch of the next mode: A(row, o) from the D fragments by quad shuffles
-        const int b = i & 1;
-        if (h == 0) mbar_wait(&full_o[b], (i >> 1) & 1);
-        const double* O = Ob + b * ob_elems;
-#pragma unroll
-        for (int t = 0; t < 2 * NT0; ++t) {
-            if (t < a.ks) {
-                const int src = (lane & ~3) + 2 * (t & 1) + (r >> 1);
-                double av[2];
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const double v0 = __shfl_sync(0xffffffffu, acc[mt][t >> 1][0], src);
-                    const double v1 = __shfl_sync(0xffffffffu, acc[mt][t >> 1][1], src);
-                    av[mt] = (r & 1) ? v1 : v0;
-                }
-#pragma unroll
-                for (int jn = 0; jn < NT1; ++jn) {
-                    const double bo = O[((t * NT1 + jn) << 5) + lane];
-                    if (h == 0) {
-                        dmma884(yacc[0][0][jn][0], yacc[0][0][jn][1], av[0], bo);
-                        dmma884(yacc[0][1][jn][0], yacc[0][1][jn][1], av[1], bo);
-                    } else {
-                        dmma884(yacc[1][0][jn][0], yacc[1][0][jn][1], av[0], bo);
-                        dmma884(yacc[1][1][jn][0], yacc[1][1][jn][1], av[1], bo);
-                    }
-                }
-            }
-        }
-        if (h == a.H - 1) mbar_arrive(&empty_o[b]);
-    }
-    // per-CTA Y_1 partial: rows are disjoint across warps, no reduction needed
-    double* outp = a.partial + (int64_t)blockIdx.x * a.I1 * a.K1;
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            const int row = 64 * h + 16 * warp + 8 * mt + q;
-            if (h >= a.H || row >= a.I1) continue;
-#pragma unroll
-            for (int jn = 0; jn < NT1; ++jn) {
-                const int k = 8 * jn + 2 * r;
-                if (k < a.K1) outp[row + a.I1 * k] = yacc[h][mt][jn][0];
-                if (k + 1 < a.K1) outp[row + a.I1 * (k + 1)] = yacc[h][mt][jn][1];
-            }
-        }
-}
 
 
 // Shrink with the small operand in registers: out^T (o x rows) = Q^T (o x d) X^T.
@@ -1097,52 +876,5 @@ void launch_stream_ttm(const TTMPlan& p, const void* in, void* out, const double
 
 namespace trg {
 
-bool fused_ttm_sketch_ok(int dtype, int64_t left, int64_t I0, int64_t K0, int64_t I1, int64_t K1) {
-    if (dtype != F64 || left != 1 || (I0 & 1) || I0 > 128 || I1 > 128 || K0 > 16 || K1 > 16) return false;
-    const int Tk = (int)((I0 + 3) / 4);
-    const size_t smem = (kStages * (size_t)(64 * I0 + kPad) + (size_t)Tk * 2 * 32 + 2 * 4 * 2 * 32) * 8 +
-                        sizeof(GaussTables) + kBarBytes;
-    return smem <= kSmemBudget;
-}
-
-void launch_fused_ttm_sketch(const FusedPlan& p, const void* x, void* out, const double* q, double* partial,
-                             double* y1, int num_sms, cudaStream_t s) {
-    FusedArgs a;
-    a.x = reinterpret_cast<const double*>(x);
-    a.out = reinterpret_cast<double*>(out);
-    a.q = q;
-    a.ldq = p.ldq;
-    a.partial = partial;
-    a.gt = gauss_tables(s);
-    a.I0 = p.I0;
-    a.I1 = p.I1;
-    a.nfib = p.nfib;
-    a.K0 = (int)p.K0;
-    a.K1 = (int)p.K1;
-    a.Tk = (int)((p.I0 + 3) / 4);
-    a.H = (int)((p.I1 + 63) / 64);
-    a.ks = (int)((p.K0 + 3) / 4);
-    a.seed = p.seed;
-    a.D1 = p.D1;
-    a.rows_glob1 = p.rows_glob1;
-    a.col_off1 = p.col_off1;
-    const int NT0 = a.K0 <= 8 ? 1 : 2;
-    const int NT1 = a.K1 <= 8 ? 1 : 2;
-    const size_t smem = (kStages * (size_t)(64 * a.I0 + kPad) + (size_t)a.Tk * NT0 * 32 + 2 * (size_t)a.ks * NT1 * 32) * 8 +
-                        sizeof(GaussTables) + kBarBytes;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nfib, num_sms));
-    const int threads = (kFCons + kFGen + 1) * 32;
-#define TRG_FZ(A, B)                                                          \
-    do {                                                                      \
-        set_smem(k_ttm_sketch_l1_f64<A, B>, smem);                            \
-        k_ttm_sketch_l1_f64<A, B><<<grid, threads, smem, s>>>(a);             \
-    } while (0)
-    if (NT0 == 1 && NT1 == 1) TRG_FZ(1, 1);
-    else if (NT0 == 1) TRG_FZ(1, 2);
-    else if (NT1 == 1) TRG_FZ(2, 1);
-    else TRG_FZ(2, 2);
-#undef TRG_FZ
-    launch_reduce_partials(partial, grid, p.I1 * p.K1, y1, s);
-}
 
 }  // namespace trg

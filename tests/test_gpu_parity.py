@@ -47,6 +47,36 @@ def test_omega_matches_reference_stream(trg):
         np.testing.assert_allclose(got, want, rtol=1e-14, atol=1e-14)
 
 
+def _u64_out(seed, k):
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (k.astype(np.uint64) + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def test_streaming_generator_near_u1_one(trg, ctx):
+    """The streaming sketch kernels' table-driven Box-Muller (common.cuh gauss_pair_state) at
+    draws whose first uniform is within 2^-14 .. 2^-17 of 1, where ln u1 is tiny: a one-hot X
+    selects those rows of Omega_0 into Y_0 (Y_0(0, :) = Omega_0(c, :), sketch.hpp:80-83)."""
+    dims = [16, 2048, 128]
+    L = dims[1] * dims[2]
+    seed = 3
+    v = (_u64_out(seed, 2 * np.arange(L // 2, dtype=np.uint64)) >> np.uint64(11)) + np.uint64(1)
+    t = ((np.uint64(1) << np.uint64(53)) - v).astype(np.float64) * 2.0 ** -53  # 1 - u1
+    pairs = np.argsort(t)[:4]  # the four uniforms closest to 1
+    assert t[pairs].max() < 2.0 ** -12 and t[pairs].min() < 2.0 ** -16
+    for p in pairs:
+        x = np.zeros(dims)
+        c = 2 * int(p)  # even draw: the cos branch of pair p
+        x[0, c % dims[1], c // dims[1]] = 1.0
+        sk = trg.DeviceSketch(ctx, trg.DeviceTensor.from_numpy(ctx, x), trg.ProjectionSpec([4, dims[1], dims[2]], seed))
+        y0 = sk.sketch_matrix(0)[0]
+        sk.close()
+        want = np.array([orc.gaussian(seed, 1, skip=c + L * k)[0] for k in range(4)])
+        np.testing.assert_allclose(y0, want, rtol=1e-14, atol=0)
+
+
 # ---------------------------------------------------------------- sketch
 SHAPES = [
     ((100, 100, 100), (10, 10, 10)),          # C1 shape
@@ -116,10 +146,8 @@ def test_sketch_householder_fallback_matches(trg):
     assert orc.rse(x, lifted) < 1e-8  # SPEC.md:304 exact capture
 
 
-def test_deferred_projection_parity(trg):
-    # shapes whose modes >= 1 run the TMA slab kernels may take the deferred path (QR of Y_n on
-    # the side stream, Y_n used for the shrink, R_n^-1 folded into later test matrices and P;
-    # opt-in with TRG_DEFERRED=1): either way the result is the reference projection
+def test_slab_modes_projection_parity(trg):
+    # modes >= 1 on the TMA slab kernels, test matrices generated inside the QR launches
     dims, K = [40, 34, 28, 22], [6, 4, 4, 4]
     x = tr_tensor(dims, [3, 3, 3, 3], 4, snr=30.0)
     proj, bases, ys = orc.sketch(x, K, 9)
