@@ -68,6 +68,7 @@ typedef struct trg_ctx trg_ctx;
 typedef struct trg_tensor trg_tensor;
 typedef struct trg_sketch trg_sketch;
 typedef struct trg_report trg_report;
+typedef struct trg_loopback trg_loopback;
 
 int trg_abi_version(void);
 const char* trg_last_error(void);
@@ -78,6 +79,19 @@ int trg_ctx_create(int device, trg_ctx** out);
 /* NCCL unique id (128 bytes) created on rank 0 and broadcast by the caller. */
 int trg_nccl_unique_id(unsigned char id[128]);
 int trg_ctx_create_dist(int device, int rank, int world, const unsigned char id[128], trg_ctx** out);
+/* Loopback communicator: `world` shard programs in ONE process, every rank on its own host
+ * thread with its own context (and stream) on `device`, usually all on the same GPU. Each
+ * collective of the sharded path (the Y_n partial sums, the padded last-mode gather, the P
+ * sum, the RSE and synthesis norms) becomes: every rank finishes its stream, a host barrier,
+ * every rank sums the `world` buffers in rank order into a private buffer (one kernel on its
+ * own stream), a second barrier, then the result replaces the rank's buffer. No kernel ever
+ * waits on another rank's kernel. It runs the sharded CUDA path exactly as the NCCL contexts
+ * do (real column offsets, uneven shards, the world > 1 QR and scatter paths) on one device,
+ * for tests; it is not a performance path. A failing rank leaves the others blocked in the
+ * next collective: callers run ranks under a timeout. */
+int trg_loopback_create(int world, trg_loopback** out);
+int trg_loopback_destroy(trg_loopback* group);
+int trg_ctx_create_loopback(int device, int rank, trg_loopback* group, trg_ctx** out);
 int trg_ctx_destroy(trg_ctx* ctx);
 int trg_ctx_synchronize(trg_ctx* ctx);
 int trg_ctx_stream(trg_ctx* ctx, void** cuda_stream);

@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     Context,
     DeviceSketch,
     DeviceTensor,
+    LoopbackGroup,
     ProjectionSpec,
     SketchResult,
     SolveReport,
@@ -23,6 +24,7 @@ from .api import (  # noqa: F401
     rse,
     rtrals,
     rtrsvd,
+    run_loopback,
     shard_range,
     sketch_offsets,
     sketch,

@@ -17,7 +17,8 @@ c_vp = ctypes.c_void_p
 # every symbol declared in include/trg.h (checked by tests/test_capi.py)
 EXPORTS = [
     "trg_abi_version", "trg_last_error", "trg_device_count",
-    "trg_ctx_create", "trg_nccl_unique_id", "trg_ctx_create_dist", "trg_ctx_destroy", "trg_ctx_synchronize",
+    "trg_ctx_create", "trg_nccl_unique_id", "trg_ctx_create_dist", "trg_loopback_create",
+    "trg_loopback_destroy", "trg_ctx_create_loopback", "trg_ctx_destroy", "trg_ctx_synchronize",
     "trg_ctx_stream", "trg_ctx_set_profiling", "trg_ctx_kernel_stats", "trg_ctx_kernel_labels",
     "trg_ctx_launch_count", "trg_ctx_reset_stats", "trg_shard_range", "trg_sketch_offsets",
     "trg_tensor_create", "trg_tensor_info", "trg_tensor_upload", "trg_tensor_download", "trg_tensor_device_ptr",

@@ -87,9 +87,13 @@ class Context:
     """One CUDA device (one process per GPU); optionally a rank of an NCCL group
     in which tensors are sharded along their last mode."""
 
-    def __init__(self, device=0, rank=0, world=1, nccl_id=None):
+    def __init__(self, device=0, rank=0, world=1, nccl_id=None, loopback=None):
         self._h = ctypes.c_void_p()
-        if world == 1:
+        if loopback is not None:
+            L.call("trg_ctx_create_loopback", ctypes.c_int(device), ctypes.c_int(rank), loopback.handle,
+                   ctypes.byref(self._h))
+            world = loopback.world
+        elif world == 1:
             L.call("trg_ctx_create", ctypes.c_int(device), ctypes.byref(self._h))
         else:
             buf = (ctypes.c_ubyte * 128).from_buffer_copy(bytes(nccl_id))
@@ -162,6 +166,69 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """trg_loopback (include/trg.h): `world` ranks of the sharded path in this process, one host
+    thread and one Context(loopback=group) each, all on one device. Collectives are host
+    barriers around rank-ordered same-device reductions; for tests of the sharded CUDA path."""
+
+    def __init__(self, world):
+        self._h = ctypes.c_void_p()
+        L.call("trg_loopback_create", ctypes.c_int(world), ctypes.byref(self._h))
+        self.world = world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            L.call("trg_loopback_destroy", self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_loopback(world, fn, device=0, timeout=900.0):
+    """fn(ctx, rank) on `world` loopback ranks (one thread and one context each); returns the
+    list of results in rank order and re-raises the first rank's exception. ctypes releases
+    the GIL inside every libtrg call, so the ranks' host code runs concurrently."""
+    import threading
+
+    group = LoopbackGroup(world)
+    out, err = [None] * world, [None] * world
+
+    def body(r):
+        ctx = None
+        try:
+            ctx = Context(device, r, loopback=group)
+            out[r] = fn(ctx, r)
+        except BaseException as e:  # noqa: BLE001 - reported to the caller below
+            err[r] = e
+        finally:
+            if ctx is not None:
+                try:
+                    ctx.close()
+                except Exception:
+                    pass
+
+    ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+    if any(t.is_alive() for t in ts):
+        raise TimeoutError(f"loopback ranks still running after {timeout} s: {[e for e in err if e]}")
+    group.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
 
 
 def shard_range(extent, rank, world):
@@ -262,7 +329,7 @@ class DeviceSketch:
 
     def __init__(self, ctx, x, spec, variant=L.TRG_SEQUENTIAL):
         self.ctx = ctx
-        self._x = x  # the projection may be recomputed from x when first read (deferred mode)
+        self._x = x  # keeps the input alive while the enqueued projection reads it
         self.dims = list(x.shape)
         self.K = [int(k) for k in spec.sketch_dims]
         self._h = ctypes.c_void_p()
@@ -504,7 +571,7 @@ def _report(h, dims):
 def decompose(x, method, cfg, spec, variant=L.TRG_SEQUENTIAL, ctx=None):
     """randomized_decompose (sketch.hpp:126-147). x: DeviceTensor (device-resident) or a host
     array (the H2D copy is then part of the call, trg_decompose_host)."""
-    ctx = ctx or default_context()
+    ctx = ctx or (x.ctx if isinstance(x, DeviceTensor) else default_context())
     m = L.TRG_ALS if method in ("als", L.TRG_ALS) else L.TRG_SVD
     dims = list(x.shape)
     if len(spec.sketch_dims) != len(dims):

@@ -178,6 +178,11 @@ void launch_minmax(const void* x, int dtype, int64_t n, double* block_mm, int nb
 void launch_affine(void* x, int dtype, int64_t n, double a, double b, cudaStream_t s);
 // dtype conversion helpers
 void launch_convert(const void* in, int in_dt, void* out, int out_dt, int64_t n, cudaStream_t s);
+// out[i] = op over ranks r = 0..nranks-1, in rank order, of ((T*)bufs[r])[i]; op 0 sum, 1 max.
+// Loopback communicator (runtime.cpp): every rank's buffer is on the same device.
+constexpr int kMaxLoopbackRanks = 16;
+void launch_rank_reduce(const void* const* bufs, int nranks, size_t count, int dtype, int op, void* out,
+                        cudaStream_t s);
 // scatter rows [lo, lo+rows) of a (rows x k) column-major matrix into a zeroed (m x k) matrix
 void launch_scatter_rows(const double* in, int64_t rows, int k, int64_t lo, int64_t m, double* out, cudaStream_t s);
 

@@ -23,11 +23,13 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <iostream>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -124,6 +126,29 @@ Nccl& nccl() {
 
 }  // namespace
 
+// ------------------------------------------------------------------ loopback communicator
+// `world` ranks of one process (one host thread and one context each, trg.h). A collective is
+// two host barriers around a rank-ordered reduction that every rank computes for itself.
+struct trg_loopback {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    std::vector<const void*> bufs;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const uint64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
 // ------------------------------------------------------------------ context
 struct KStat {
     double ms = 0.0;
@@ -138,6 +163,7 @@ struct trg_ctx {
     cudaStream_t side = nullptr;  // test-matrix generation for later modes, overlapped with QR / shrink
     cudaMemPool_t pool = nullptr;  // private stream-ordered pool (release threshold: keep)
     ncclComm_t comm = nullptr;
+    trg_loopback* lb = nullptr;  // loopback ranks (no NCCL): see reduce_loopback
     bool profiling = false;
     int64_t launches = 0;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -235,12 +261,29 @@ struct trg_ctx {
     }
     void allreduce(void* buf, size_t count, int dtype) {
         if (world == 1 || count == 0) return;
+        if (lb) return reduce_loopback(buf, count, dtype, 0);
         nccl().check(nccl().allReduce(buf, buf, count, dtype == F64 ? ncclFloat64 : ncclFloat32, ncclSum, comm, stream),
                      "ncclAllReduce");
     }
     void allreduce_op(void* buf, size_t count, ncclRedOp_t op) {
         if (world == 1 || count == 0) return;
+        if (lb) return reduce_loopback(buf, count, F64, op == ncclMax ? 1 : 0);
         nccl().check(nccl().allReduce(buf, buf, count, ncclFloat64, op, comm, stream), "ncclAllReduce");
+    }
+    // The loopback allreduce: the same device holds every rank's buffer, so after a barrier each
+    // rank reduces all of them in rank order into a private buffer; after a second barrier (no
+    // rank reads the others' buffers any more) the result replaces its own.
+    void reduce_loopback(void* buf, size_t count, int dtype, int op) {
+        const size_t bytes = count * trg::dtype_size(dtype);
+        CK(cudaStreamSynchronize(stream));
+        lb->bufs[rank] = buf;
+        lb->barrier();
+        void* out = alloc(bytes);
+        launch("allreduce", [&] { trg::launch_rank_reduce(lb->bufs.data(), world, count, dtype, op, out, stream); });
+        CK(cudaStreamSynchronize(stream));
+        lb->barrier();
+        CK(cudaMemcpyAsync(buf, out, bytes, cudaMemcpyDeviceToDevice, stream));
+        dfree(out);
     }
 };
 
@@ -1186,6 +1229,33 @@ int trg_ctx_create_dist(int device, int rank, int world, const unsigned char id[
             std::memcpy(u.internal, id, 128);
             nccl().check(nccl().commInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
         }
+        *out = c.release();
+    });
+}
+
+int trg_loopback_create(int world, trg_loopback** out) {
+    return guard([&] {
+        require(world >= 1 && world <= trg::kMaxLoopbackRanks, "loopback: world must be in [1, 16]");
+        auto g = std::make_unique<trg_loopback>();
+        g->world = world;
+        g->bufs.assign(world, nullptr);
+        *out = g.release();
+    });
+}
+
+int trg_loopback_destroy(trg_loopback* g) {
+    return guard([&] { delete g; });
+}
+
+int trg_ctx_create_loopback(int device, int rank, trg_loopback* g, trg_ctx** out) {
+    return guard([&] {
+        require(g != nullptr, "loopback: null group");
+        require(rank >= 0 && rank < g->world, "ctx: bad rank/world");
+        auto c = std::make_unique<trg_ctx>();
+        ctx_init(c.get(), device);
+        c->rank = rank;
+        c->world = g->world;
+        c->lb = g;
         *out = c.release();
     });
 }

@@ -257,11 +257,7 @@ __global__ void k_omega(uint64_t seed, uint64_t off, int64_t n, double* out, con
 
 template <typename T, int TD, int TK, bool L1>
 void set_smem_attr(size_t smem) {
-    static size_t done = 0;
-    if (smem > 48 * 1024 && smem > done) {
-        cudaFuncSetAttribute(k_sketch<T, TD, TK, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        done = smem;
-    }
+    allow_smem(k_sketch<T, TD, TK, L1>, smem);
 }
 
 template <typename T, int TD, int TK>
@@ -350,6 +346,9 @@ const GaussTables* gauss_tables(cudaStream_t s) {
         GaussTables* t = nullptr;
         if (cudaMalloc(&t, sizeof(GaussTables)) != cudaSuccess) return nullptr;
         k_gauss_tables<<<1, 256, 0, s>>>(t);
+        // other host threads (contexts on other streams) may read the tables as soon as they see
+        // the pointer: finish building them first (once per device)
+        if (cudaStreamSynchronize(s) != cudaSuccess) return nullptr;
         per_dev[dev] = t;
     }
     return per_dev[dev];

@@ -355,8 +355,7 @@ void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, dou
     const int threads = (kCons + kProd + kRng) * 32;
 #define TRG_SL(MTV, NTV)                                                                                   \
     do {                                                                                                   \
-        cudaFuncSetAttribute(k_slab_sketch_f64<MTV, NTV>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                             (int)smem);                                                                   \
+        allow_smem(k_slab_sketch_f64<MTV, NTV>, smem);                                                    \
         k_slab_sketch_f64<MTV, NTV><<<grid, threads, smem, s>>>(a);                                        \
     } while (0)
 #define TRG_SL_NT(MTV)                   \
@@ -403,19 +402,19 @@ void launch_slab_ttm(const TTMPlan& p, const void* in, void* out, const double* 
     const int threads = (kCons + kProd) * 32;
     switch (NT) {
         case 1:
-            cudaFuncSetAttribute(k_slab_ttm_f64<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            allow_smem(k_slab_ttm_f64<1>, smem);
             k_slab_ttm_f64<1><<<grid, threads, smem, s>>>(a);
             break;
         case 2:
-            cudaFuncSetAttribute(k_slab_ttm_f64<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            allow_smem(k_slab_ttm_f64<2>, smem);
             k_slab_ttm_f64<2><<<grid, threads, smem, s>>>(a);
             break;
         case 4:
-            cudaFuncSetAttribute(k_slab_ttm_f64<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            allow_smem(k_slab_ttm_f64<4>, smem);
             k_slab_ttm_f64<4><<<grid, threads, smem, s>>>(a);
             break;
         default:
-            cudaFuncSetAttribute(k_slab_ttm_f64<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            allow_smem(k_slab_ttm_f64<8>, smem);
             k_slab_ttm_f64<8><<<grid, threads, smem, s>>>(a);
             break;
     }

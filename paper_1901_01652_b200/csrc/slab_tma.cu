@@ -445,7 +445,7 @@ size_t slab_smem(size_t stage, int S) { return (size_t)S * stage + 2 * S * 8 + 1
 
 template <typename KernelT>
 void set_smem(KernelT k, size_t smem) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(k, smem);
 }
 
 }  // namespace

@@ -510,12 +510,12 @@ int launch_stream_sketch_f32(const SketchPlan& sp, const void* x, double* partia
 #define TRG_F32(TKV)                                                                                          \
     do {                                                                                                      \
         constexpr int G = TKV <= 12 ? TRG_F32_GEN_SMALL : TRG_F32_GEN_LARGE;                                  \
-        cudaFuncSetAttribute(k_sketch_l1_f32<TKV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem); \
+        allow_smem(k_sketch_l1_f32<TKV, G>, p.smem); \
         k_sketch_l1_f32<TKV, G><<<grid, (kF32Cons + G + 1) * 32, p.smem, s>>>(map, a);                        \
     } while (0)
     if (p.nkb > 1) {  // several k-blocks per tile: the Box-Muller generation is the bound
         constexpr int G = TRG_F32_GEN_MULTI;
-        cudaFuncSetAttribute(k_sketch_l1_f32<16, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        allow_smem(k_sketch_l1_f32<16, G>, p.smem);
         k_sketch_l1_f32<16, G><<<grid, (kF32Cons + G + 1) * 32, p.smem, s>>>(map, a);
         if (y) launch_reduce_partials(partial, gc, sp.dim * sp.K, y, s);
         return gc;
@@ -573,7 +573,7 @@ void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const do
     const int threads = (kTtCons + 1) * 32;
 #define TRG_TT(KPV)                                                                                     \
     do {                                                                                                \
-        cudaFuncSetAttribute(k_ttm_l1_f32<KPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        allow_smem(k_ttm_l1_f32<KPV>, smem); \
         k_ttm_l1_f32<KPV><<<grid, threads, smem, s>>>(map, a, q, ldq);                                  \
     } while (0)
     switch (a.Kp) {

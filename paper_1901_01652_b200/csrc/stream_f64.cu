@@ -682,7 +682,7 @@ int nt_for(int K) {
 
 template <typename KernelT>
 void set_smem(KernelT k, size_t smem) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(k, smem);
 }
 
 constexpr size_t kSmemBudget = 220 * 1024;

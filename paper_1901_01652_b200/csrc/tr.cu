@@ -319,4 +319,31 @@ void launch_scatter_rows(const double* in, int64_t rows, int k, int64_t lo, int6
     k_scatter_rows<<<grid_for(m * k), 256, 0, s>>>(in, rows, k, lo, m, out);
 }
 
+// ---- loopback communicator: rank-ordered reduction of same-device buffers
+struct RankBufs {
+    const void* p[kMaxLoopbackRanks];
+};
+
+template <typename T>
+__global__ void k_rank_reduce(RankBufs b, int nranks, int64_t n, int op, T* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T acc = static_cast<const T*>(b.p[0])[i];
+        for (int r = 1; r < nranks; ++r) {
+            const T v = static_cast<const T*>(b.p[r])[i];
+            acc = op == 0 ? acc + v : (v > acc ? v : acc);
+        }
+        out[i] = acc;
+    }
+}
+
+void launch_rank_reduce(const void* const* bufs, int nranks, size_t count, int dtype, int op, void* out,
+                        cudaStream_t s) {
+    RankBufs b{};
+    for (int r = 0; r < nranks; ++r) b.p[r] = bufs[r];
+    if (dtype == F64)
+        k_rank_reduce<double><<<grid_for((int64_t)count), 256, 0, s>>>(b, nranks, (int64_t)count, op, (double*)out);
+    else
+        k_rank_reduce<float><<<grid_for((int64_t)count), 256, 0, s>>>(b, nranks, (int64_t)count, op, (float*)out);
+}
+
 }  // namespace trg

@@ -140,11 +140,7 @@ __global__ void __launch_bounds__(256) k_ttm(TTMArgs a) {
 
 template <typename T, int TM, int TO, bool L1>
 void run(const TTMPlan& p, const TTMArgs& a, cudaStream_t s) {
-    static size_t done = 0;
-    if (p.smem > 48 * 1024 && p.smem > done) {
-        cudaFuncSetAttribute(k_ttm<T, TM, TO, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-        done = p.smem;
-    }
+    allow_smem(k_ttm<T, TM, TO, L1>, p.smem);
     dim3 grid(p.grid_x, p.noT, p.dsplit);
     k_ttm<T, TM, TO, L1><<<grid, p.threads, p.smem, s>>>(a);
 }
