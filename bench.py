@@ -293,11 +293,27 @@ def main():
 
     import torch
 
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N`: one process per GPU, launched here the way the driver does
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}")
+        import socket
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
+
     import paper_1901_01652_b200 as trg
     from paper_1901_01652_b200 import _lib as L
     from paper_1901_01652_b200.synthetic import make_tensor
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

@@ -85,6 +85,17 @@ bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t 
 void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
                            cudaStream_t s);
 
+// ---- fp32 mode-0 sketch / shrink on tcgen05 (kind::tf32, 3xTF32, TMEM accumulators), tc_f32.cu
+bool tc_sketch_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
+int tc_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms);  // = partial count
+int launch_tc_sketch_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                         cudaStream_t s);
+bool tc_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols);
+size_t tc_ttm_f32_scratch(int64_t dim, int64_t K);  // bytes of the split Q operand
+// out: P^(1) in fp64 (f64_out) or fp32; q: Q (ldq x K column-major fp64)
+void launch_tc_ttm_f32(const TTMPlan& p, const void* in, void* out, bool f64_out, const double* q, int64_t ldq,
+                       float* scratch, int num_sms, cudaStream_t s);
+
 // ---- cp.async-gathered fp64 tensor-core kernels for modes with left > 1 (slab_f64.cu)
 bool slab_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
 void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,

@@ -463,6 +463,13 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
             trg::launch_stream_sketch(p, cur, partial, yout, ctx->num_sms, &grid, ctx->stream);
         }, yout ? 2 : 1);
         if (defer) *yp = YParts{partial, grid};
+    } else if (trg::tc_sketch_f32_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
+        const int gc = trg::tc_sketch_f32_grid(p.dim, (int)Kn, p.right, ctx->num_sms);
+        partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_tc_sketch_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, gc};
     } else if (trg::stream_sketch_f32_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
         int gc = 0;
         trg::stream_sketch_f32_grid(p.dim, (int)Kn, p.right, ctx->num_sms, &gc);
@@ -513,6 +520,11 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     ctx->allreduce(dYfull, (size_t)(x->dims[n] * Kn), F64);
 }
 
+// fp32 mode-0 shrinks write P^(1) in fp64 (the later modes then run the fp64 kernels)
+bool mode0_promotes(int dt, int64_t left, int64_t dim, int64_t K, int64_t right) {
+    return trg::tc_ttm_f32_ok(dt, left, dim, K, right) || trg::stream_ttm_f32_ok(dt, left, dim, K, right);
+}
+
 // out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
 // out = cur x_n Q^T; *odt is the output dtype (fp32 mode-0 input is promoted to fp64 by its shrink)
 void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, const std::vector<int64_t>& cur_shape,
@@ -532,11 +544,18 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
     p.m_sd = 1;
     const double* m = dQ;
     if (n == N - 1) m += x->lo;  // local rows of Q_{N-1}
-    const bool promote = trg::stream_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right);
+    const bool tc = trg::tc_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right);
+    const bool promote = mode0_promotes(p.dtype, p.left, p.dim, Kn, p.right);
     *odt = promote ? F64 : cdt;
     const size_t es = trg::dtype_size(*odt);
     void* out = escape ? ctx->alloc(es * (size_t)(p.left * Kn * p.right)) : ctx->tmp(es * (size_t)(p.left * Kn * p.right));
-    if (promote) {
+    if (tc) {
+        float* scratch = (float*)ctx->tmp(trg::tc_ttm_f32_scratch(p.dim, Kn));
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_tc_ttm_f32(p, cur, out, *odt == F64, m, x->dims[n], scratch, ctx->num_sms, ctx->stream);
+        }, 2);
+        ctx->tmp_free(scratch);
+    } else if (promote) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm_f32(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
         });
@@ -783,7 +802,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 // matrices (one mode per launch), in the latency-bound QR instead of next to the
                 // HBM-bound shrink
                 pre_started = true;
-                const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
+                const bool promotes = mode0_promotes(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
                 schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre, true,
                                    kr_on ? &krp.om : nullptr);
             }
@@ -794,7 +813,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 // shrink (HBM-bound, one CTA per SM with room to spare), not next to the QR or
                 // the sketch, which it would slow down
                 pre_started = true;
-                const bool promotes = trg::stream_ttm_f32_ok(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
+                const bool promotes = mode0_promotes(cdt, prod(shape, 0, n), shape[n], Kn, prod(shape, n + 1));
                 schedule_pre_omega(ctx, x, promotes ? (int)F64 : cdt, sk->K, seed, offs, n, pre, false,
                                    kr_on ? &krp.om : nullptr);
             }
