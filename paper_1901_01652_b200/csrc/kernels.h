@@ -11,6 +11,13 @@ enum DType { F32 = 0, F64 = 1 };
 
 inline size_t dtype_size(int dt) { return dt == F64 ? 8 : 4; }
 
+// Stream-ordered scratch for launchers that need a temporary (multi-CTA QR, split-d TTM): from the
+// calling context's private pool (set by trg_ctx::launch for the thread), else the device's
+// default pool.
+void set_thread_pool(cudaMemPool_t pool);
+void* scratch_alloc(size_t bytes, cudaStream_t s);
+void scratch_free(void* p, cudaStream_t s);
+
 // ---- opt-in Khatri-Rao test matrix (TRG_OMEGA_KHATRI_RAO) ----
 // Omega_n(c, k) = A(c mod left, k) * F(r mod S1, k) * H(r / S1, k), r = c / left, where A is the
 // Khatri-Rao product of the per-mode Gaussian factors of the modes before n (left x K), F the

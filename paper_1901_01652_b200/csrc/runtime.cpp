@@ -126,6 +126,22 @@ Nccl& nccl() {
 
 }  // namespace
 
+namespace trg {
+thread_local cudaMemPool_t tls_pool = nullptr;
+void set_thread_pool(cudaMemPool_t pool) { tls_pool = pool; }
+void* scratch_alloc(size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    if (tls_pool)
+        cuda_check(cudaMallocFromPoolAsync(&p, bytes ? bytes : 8, tls_pool, s), "scratch_alloc");
+    else
+        cuda_check(cudaMallocAsync(&p, bytes ? bytes : 8, s), "scratch_alloc");
+    return p;
+}
+void scratch_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+}  // namespace trg
+
 // ------------------------------------------------------------------ loopback communicator
 // `world` ranks of one process (one host thread and one context each, trg.h). A collective is
 // two host barriers around a rank-ordered reduction that every rank computes for itself.
@@ -183,6 +199,7 @@ struct trg_ctx {
     // Run one kernel launch, counted and (optionally) timed with events on the stream.
     template <typename F>
     void launch(const std::string& label, F&& f, int count = 1) {
+        trg::set_thread_pool(pool);  // launchers' own scratch comes from this context's pool
         cudaEvent_t a = nullptr, b = nullptr;
         if (profiling) {
             a = get_event();

@@ -2,11 +2,13 @@
 //
 // fp32 mode-0 sketch and shrink on the 5th-generation tensor cores (tcgen05, kind::tf32, TMEM
 // accumulators, TMA-fed shared memory), in 3xTF32: every fp32 operand v is split into
-// hi = rna_tf32(v) and lo = v - hi, and  v w  ~  hi_v hi_w + lo_v hi_w + hi_v lo_w.
-// The dropped lo_v lo_w is below 2^-22 |v w| and the lo operands are read to 11 bits
-// (2^-11 of 2^-11), so a product carries ~2^-21 relative error against fp32's 2^-24: the
-// stage stays inside the 1e-4 fp32 parity bound against the fp64 oracle with a wide margin,
-// while plain TF32 (2^-11) would not (BASELINE.json north_star).
+// hi = trunc_tf32(v) (what the tensor core reads from the raw fp32 word) and lo = v - hi (exact),
+// and  v w  ~  hi_v hi_w + lo_v hi_w + hi_v lo_w. The dropped lo_v lo_w is below 2^-20 |v w| and
+// the lo operands are read to 11 bits, so a product carries ~1e-6 relative error, random in
+// sign: the stage stays far inside the 1e-4 fp32 parity bound against the fp64 oracle, while
+// plain TF32 (2^-10 truncation) would not (BASELINE.json north_star).
+// Only lo is written to shared memory (the raw X tile is its own hi), and the tensor core reads
+// X twice (K2: hi against [Q_hi | Q_lo] concatenated along N, lo against Q_hi).
 //
 //   K1  Y_0 = X_(0) Omega_0       (sketch.hpp:80-83; unfold_classic tensor.hpp:133-142)
 //       D[I0 x K] += A[I0 x kb] B[kb x K]: A = a kb-column block of X_(0) (the I0-long mode-0
@@ -122,87 +124,137 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ float tf32_rna(float v) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-    return __uint_as_float(r);
-}
+// kind::tf32 reads an fp32 operand as its top 19 bits, i.e. TRUNCATED (measured,
+// tools/tc_probe.cu): a raw fp32 buffer is its own hi part, and lo = v - trunc(v) is exact.
+__device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
-// v -> (hi, lo) in place / beside: the 3xTF32 split of one stage buffer (layout-agnostic)
-__device__ __forceinline__ void split_stage(uint32_t hi, uint32_t lo, uint32_t bytes, int tid, int nthr) {
-    for (uint32_t o = (uint32_t)tid * 16u; o < bytes; o += (uint32_t)nthr * 16u) {
+// lo = v - trunc_tf32(v) of one stage (layout-agnostic), four 16-byte loads in flight per thread
+__device__ __forceinline__ void split_lo(uint32_t src, uint32_t lo, uint32_t bytes, int tid, int nthr) {
+    const uint32_t step = (uint32_t)nthr * 16u;
+    uint32_t o = (uint32_t)tid * 16u;
+    for (; o + 3 * step < bytes; o += 4 * step) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                         : "r"(src + o + u * step));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo + o + u * step), "f"(v[u].x - tf32_trunc(v[u].x)),
+                         "f"(v[u].y - tf32_trunc(v[u].y)), "f"(v[u].z - tf32_trunc(v[u].z)),
+                         "f"(v[u].w - tf32_trunc(v[u].w)));
+    }
+    for (; o < bytes; o += step) {
         float4 v;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(hi + o));
-        const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hi + o), "f"(h.x), "f"(h.y), "f"(h.z), "f"(h.w));
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo + o), "f"(v.x - h.x), "f"(v.y - h.y),
-                     "f"(v.z - h.z), "f"(v.w - h.w));
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(src + o));
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo + o), "f"(v.x - tf32_trunc(v.x)),
+                     "f"(v.y - tf32_trunc(v.y)), "f"(v.z - tf32_trunc(v.z)), "f"(v.w - tf32_trunc(v.w)));
     }
 }
 
 __device__ __forceinline__ void sts32(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
 
-constexpr int kWarps = 10;
-constexpr int kThreads = kWarps * 32;
 constexpr int kSplitW0 = 2, kSplitWarps = 4;  // warps 2..5
-constexpr int kAuxW0 = 6, kAuxWarps = 4;      // warps 6..9
 
 // ================================================================== K1: mode-0 sketch
+// Y_0 (I0 x K) = X_(0) Omega_0: D[M x N] += A[M x 8] B[8 x N] per k-step, A = 32-row blocks of an
+// X column block (MN-major, M = 128 per tile, or 64 when I0 <= 64), B = Omega block (K-major).
+// Rings: X (XR deep, TMA -> MMA), lo of X (2 deep, splitters -> MMA) and Omega hi / lo (BR deep,
+// generators -> MMA: the generators run ahead of the tensor core). Warps: 0 TMA, 1 MMA (+ TMEM),
+// 2-5 splitters, 6-17 generators, 18-21 drainers.
+// The tensor core's fp32 accumulation loses about one rounding per accumulation step (measured:
+// Y_0 error ~ linear in the columns a CTA accumulates, 1e-5 after ~1400 columns, 6e-4 after C5's
+// 87k), so the accumulator is drained into the CTA's fp64 partial every `seg` stages (~256
+// columns): the MMAs alternate between two TMEM accumulator sets while the drainers add the idle
+// one into the partial (RMW in L2; the CTA owns its slab). When two sets do not fit TMEM (C4: 8 x
+// 64 of 512 columns) a CTA drains once, at its end. With N-concatenation (ncat: D = A [B_hi B_lo]
+// + A_lo B_hi, two MMAs) a set is 2 Kp wide and the drain sums its halves.
+constexpr int kSkGenW0 = 6, kSkGenWarps = 12, kSkDrainW0 = 18, kSkDrainWarps = 4;
+constexpr int kSkThreads = 22 * 32;
+constexpr int kWR = 2;  // lo-ring depth
+static_assert(kSkDrainW0 + kSkDrainWarps == kSkThreads / 32 && kSkGenW0 + kSkGenWarps == kSkDrainW0, "warp roles");
+
 struct TcSkArgs {
-    int I0, K, Kp, Mt, nblk, kb, S;
+    int I0, K, Kp, M, Mt, nblk, kb, XR, BR, seg, nset, ncat, RS;  // Mt: M tiles per CTA, RS row splits
     int64_t L, ntiles;
     uint64_t seed, D;
     int64_t rows_glob, col_off;
     double* partial;  // per CTA: I0 x K fp64, column-major
-    const GaussTables* gt;
-    uint32_t a_bytes, b_bytes;  // per-stage A (X block) and B (one of hi / lo) buffer sizes
-    float* dbg;                 // development probe (TRG_TC_DEBUG), normally null
+    uint32_t a_bytes, b_bytes;  // X block (M-padded) and one of B hi / lo
+    long long* prof;  // development timeline (TRG_TC_PROF): CTA 0, 8 stamps x 256 stages
 };
+#define TC_STAMP(slot, j)                                                        \
+    do {                                                                         \
+        if (a.prof && blockIdx.x == 0 && (j) < 256) a.prof[(slot) * 256 + (j)] = clock64(); \
+    } while (0)
 
 // B element (n, c) of a stage, K-major no-swizzle: core matrices of 8 rows x 16 bytes, the two
-// 4-column halves of a k-step LBO = 128 B apart, 8-row groups SBO = 256 B apart, k-steps Kp*32 B
-__device__ __forceinline__ uint32_t b_off(int n, int c, int Kp) {
-    return (uint32_t)((c >> 3) * Kp * 32 + (n >> 3) * 256 + ((c >> 2) & 1) * 128 + (n & 7) * 16 + (c & 3) * 4);
+// 4-column halves of a k-step LBO = 128 B apart, 8-row groups SBO = 256 B apart; k-step blocks
+// of NB rows (2 Kp with N-concatenation: B_lo rows follow B_hi's) NB * 32 B apart
+__device__ __forceinline__ uint32_t b_off(int n, int c, int NB) {
+    return (uint32_t)((c >> 3) * NB * 32 + (n >> 3) * 256 + ((c >> 2) & 1) * 128 + (n & 7) * 16 + (c & 3) * 4);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_tc_sketch_f32(const __grid_constant__ CUtensorMap xmap, TcSkArgs a) {
+__global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_constant__ CUtensorMap xmap, TcSkArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // ---- carve: [stages: A hi | A lo | B hi | B lo] (1024-aligned) | tables | barriers
+    // ---- carve (1024-aligned): X ring | lo ring | B ring [hi | lo] | barriers
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
-    const uint32_t stage_bytes = 2 * a.a_bytes + 2 * a.b_bytes;
-    GaussTables* tabs = reinterpret_cast<GaussTables*>(gbase + (size_t)a.S * stage_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(tabs) + sizeof(GaussTables));
-    uint64_t* full = bars;               // TMA landed (expect_tx)
-    uint64_t* split = bars + a.S;        // X split into hi / lo (kSplitWarps arrivals)
-    uint64_t* omega = bars + 2 * a.S;    // B generated (kAuxWarps arrivals)
-    uint64_t* empty = bars + 3 * a.S;    // MMAs of the stage done (tcgen05.commit)
-    uint64_t* done = bars + 4 * a.S;     // every MMA done
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * a.S + 1);
-    auto A_hi = [&](int s) { return base + (uint32_t)s * stage_bytes; };
-    auto A_lo = [&](int s) { return A_hi(s) + a.a_bytes; };
-    auto B_hi = [&](int s) { return A_hi(s) + 2 * a.a_bytes; };
-    auto B_lo = [&](int s) { return B_hi(s) + a.b_bytes; };
+    const uint32_t lbase = base + (uint32_t)a.XR * a.a_bytes;
+    const uint32_t bbase = lbase + (uint32_t)kWR * a.a_bytes;
+    const uint32_t ring_bytes = (uint32_t)(a.XR + kWR) * a.a_bytes + (uint32_t)a.BR * 2u * a.b_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + ring_bytes);
+    uint64_t* xfull = bars;                  // [XR] TMA landed
+    uint64_t* xempty = xfull + a.XR;         // [XR] MMAs done with the X slot
+    uint64_t* wsplit = xempty + a.XR;        // [2] lo written
+    uint64_t* wempty = wsplit + kWR;         // [2] MMAs done with the lo slot
+    uint64_t* bfull = wempty + kWR;          // [BR] Omega block written
+    uint64_t* bempty = bfull + a.BR;         // [BR] MMAs done with the Omega slot
+    uint64_t* dfull = bempty + a.BR;         // [2] accumulator set ready to drain
+    uint64_t* dempty = dfull + 2;            // [2] accumulator set drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
+    auto X = [&](int r) { return base + (uint32_t)r * a.a_bytes; };
+    auto LO = [&](int w) { return lbase + (uint32_t)w * a.a_bytes; };
+    auto BH = [&](int b) { return bbase + (uint32_t)b * 2u * a.b_bytes; };
+    auto BL = [&](int b) { return BH(b) + a.b_bytes; };  // with ncat: rows Kp.. of one B block
+    const int NB = a.ncat ? 2 * a.Kp : a.Kp;              // rows of a B k-step block
 
-    // this CTA's tiles (kb columns each): a contiguous range
-    const int64_t t0 = a.ntiles * blockIdx.x / gridDim.x, t1 = a.ntiles * (blockIdx.x + 1) / gridDim.x;
+    // CTA = (column group cg, row split rs): rows [rs Mt M, (rs + 1) Mt M) of the column group's
+    // columns (C3 / C4 split their rows so that two N-concatenated accumulator sets fit TMEM;
+    // the RS CTAs of a column group regenerate the same test-matrix block)
+    const int rs = blockIdx.x % a.RS, cg = blockIdx.x / a.RS, ncg = gridDim.x / a.RS;
+    const int bpt = a.M / 32;  // 32-row blocks per M tile
+    const int blk0 = rs * a.Mt * bpt;
+    const int nbc = max(0, min(a.nblk - blk0, a.Mt * bpt));  // real blocks of this CTA
+    const int64_t t0 = a.ntiles * cg / ncg, t1 = a.ntiles * (cg + 1) / ncg;
     const int nt = (int)(t1 - t0);
-    const uint32_t tcols = a.Mt * a.Kp <= 32 ? 32u : a.Mt * a.Kp <= 64 ? 64u : a.Mt * a.Kp <= 128 ? 128u
-                                                                               : a.Mt * a.Kp <= 256 ? 256u : 512u;
+    const int nseg = (nt + a.seg - 1) / a.seg;
+    const uint32_t setcols = (uint32_t)(a.Mt * (a.ncat ? 2 : 1) * a.Kp);
+    const uint32_t need = setcols * (uint32_t)a.nset;
+    const uint32_t tcols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
 
-    // ---- set-up: zero every stage (padding rows / columns stay zero), tables, barriers, TMEM
-    for (uint32_t o = threadIdx.x * 16u; o < (uint32_t)a.S * stage_bytes; o += kThreads * 16u)
+    // ---- set-up: zero both rings (padding rows / columns stay zero), barriers, TMEM
+    for (uint32_t o = threadIdx.x * 16u; o < ring_bytes; o += kSkThreads * 16u)
         asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + o), "r"(0u));
-    gauss_tables_to_smem(*tabs, a.gt);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < a.S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&split[s], kSplitWarps);
-            mbar_init(&omega[s], kAuxWarps);
-            mbar_init(&empty[s], 1);
+        for (int r = 0; r < a.XR; ++r) {
+            mbar_init(&xfull[r], 1);
+            mbar_init(&xempty[r], 1);
         }
-        mbar_init(done, 1);
+        for (int w = 0; w < kWR; ++w) {
+            mbar_init(&wsplit[w], kSplitWarps);
+            mbar_init(&wempty[w], 1);
+        }
+        for (int b = 0; b < a.BR; ++b) {
+            mbar_init(&bfull[b], kSkGenWarps);
+            mbar_init(&bempty[b], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&dfull[b], 1);
+            mbar_init(&dempty[b], kSkDrainWarps);
+        }
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, tcols);
@@ -211,153 +263,195 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_sketch_f32(const __grid_cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t lbo_a = (uint32_t)a.kb * 128u;  // 32-row blocks of A
 
     if (warp == 0) {
-        // ================= TMA producer
+        // ================= TMA producer (X ring)
         if (lane == 0) {
             const uint64_t pol = policy_l2(0);
             for (int j = 0; j < nt; ++j) {
-                const int s = j % a.S;
-                if (j >= a.S) mbar_wait(&empty[s], ((j / a.S) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], (uint32_t)a.nblk * (uint32_t)a.kb * 128u);
+                const int r = j % a.XR;
+                TC_STAMP(0, j);
+                if (j >= a.XR) mbar_wait(&xempty[r], ((j / a.XR) - 1) & 1);
+                TC_STAMP(1, j);
+                mbar_arrive_expect_tx(&xfull[r], (uint32_t)nbc * lbo_a);
                 const int c0 = (int)((t0 + j) * a.kb);
-                for (int b = 0; b < a.nblk; ++b)
-                    tma2d(A_hi(s) + (uint32_t)b * (uint32_t)a.kb * 128u, &xmap, 32 * b, c0, &full[s], pol);
+                for (int b = 0; b < nbc; ++b)
+                    tma2d(X(r) + (uint32_t)b * lbo_a, &xmap, 32 * (blk0 + b), c0, &xfull[r], pol);
             }
         }
     } else if (warp == 1) {
         // ================= MMA issuer
-        const uint32_t idesc = idesc_tf32(128, a.Kp, /*a MN-major*/ 1, /*b K-major*/ 0);
-        const uint32_t lbo_a = (uint32_t)a.kb * 128u;  // 32-row blocks of A
-        for (int j = 0; j < nt; ++j) {
-            const int s = j % a.S;
-            const uint32_t ph = (j / a.S) & 1;
-            mbar_wait(&full[s], ph);
-            mbar_wait(&split[s], ph);
-            mbar_wait(&omega[s], ph);
+        const uint32_t idesc1 = idesc_tf32(a.M, NB, /*a MN-major*/ 1, /*b K-major*/ 0);
+        const uint32_t idesc2 = idesc_tf32(a.M, a.Kp, 1, 0);
+        for (int g = 0; g < nseg; ++g) {
+            const int set = g % a.nset;
+            if (g >= a.nset) mbar_wait(&dempty[set], ((g / a.nset) - 1) & 1);
             tc_fence_after();
-            if (lane == 0) {
-                for (int ks = 0; ks < a.kb / 8; ++ks) {
-                    const uint64_t bh = sdesc(B_hi(s) + (uint32_t)ks * a.Kp * 32u, 128, 256, kSwNone);
-                    const uint64_t bl = sdesc(B_lo(s) + (uint32_t)ks * a.Kp * 32u, 128, 256, kSwNone);
-                    for (int mt = 0; mt < a.Mt; ++mt) {
-                        // tf32 MN-major operands take the 128B swizzle of 32-byte chunks (the only
-                        // MN-major tf32 layout): 4-row groups SBO = 512 B apart, 8 rows per k-step
-                        const uint32_t aoff = (uint32_t)mt * 4u * lbo_a + (uint32_t)ks * 1024u;
-                        const uint64_t ah = sdesc(A_hi(s) + aoff, lbo_a, 512, kSw128b32);
-                        const uint64_t al = sdesc(A_lo(s) + aoff, lbo_a, 512, kSw128b32);
-                        const uint32_t d = tmem + (uint32_t)(mt * a.Kp);
-                        const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
-                        mma_tf32(d, ah, bh, idesc, acc);
-                        mma_tf32(d, al, bh, idesc, 1u);
-                        mma_tf32(d, ah, bl, idesc, 1u);
+            const int j1 = min(nt, (g + 1) * a.seg);
+            for (int j = g * a.seg; j < j1; ++j) {
+                const int r = j % a.XR, w = j % kWR, bq = j % a.BR;
+                mbar_wait(&xfull[r], (j / a.XR) & 1);
+                if (lane == 0) TC_STAMP(2, j);
+                mbar_wait(&wsplit[w], (j / kWR) & 1);
+                mbar_wait(&bfull[bq], (j / a.BR) & 1);
+                if (lane == 0) TC_STAMP(3, j);
+                tc_fence_after();
+                if (lane == 0) {
+                    for (int ks = 0; ks < a.kb / 8; ++ks) {
+                        const uint64_t bh = sdesc(BH(bq) + (uint32_t)ks * NB * 32u, 128, 256, kSwNone);
+                        const uint64_t bl = sdesc(BL(bq) + (uint32_t)ks * a.Kp * 32u, 128, 256, kSwNone);
+                        for (int mt = 0; mt < a.Mt; ++mt) {
+                            // tf32 MN-major operands take the 128B swizzle of 32-byte chunks (the
+                            // only MN-major tf32 layout): 4-row groups SBO = 512 B apart, 8 rows per k-step
+                            const uint32_t aoff = (uint32_t)mt * 4u * lbo_a + (uint32_t)ks * 1024u;
+                            const uint64_t ah = sdesc(X(r) + aoff, lbo_a, 512, kSw128b32);
+                            const uint64_t al = sdesc(LO(w) + aoff, lbo_a, 512, kSw128b32);
+                            const uint32_t d = tmem + (uint32_t)set * setcols + (uint32_t)(mt * (a.ncat ? 2 : 1) * a.Kp);
+                            const uint32_t acc = (j > g * a.seg || ks > 0) ? 1u : 0u;
+                            mma_tf32(d, ah, bh, idesc1, acc);  // hi [B_hi (B_lo)]
+                            mma_tf32(d, al, bh, idesc2, 1u);   // lo B_hi
+                            if (!a.ncat) mma_tf32(d, ah, bl, idesc2, 1u);
+                        }
+                    }
+                    mma_commit(&xempty[r]);
+                    mma_commit(&wempty[w]);
+                    mma_commit(&bempty[bq]);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mma_commit(&dfull[set]);
+            __syncwarp();
+        }
+    } else if (warp >= kSplitW0 && warp < kSplitW0 + kSplitWarps) {
+        // ================= X splitters: lo = X - trunc_tf32(X) into the work ring
+        const int tid = threadIdx.x - kSplitW0 * 32;
+        const uint32_t real = (uint32_t)nbc * lbo_a;
+        for (int j = 0; j < nt; ++j) {
+            const int r = j % a.XR, w = j % kWR;
+            if (j >= kWR) mbar_wait(&wempty[w], ((j / kWR) - 1) & 1);
+            mbar_wait(&xfull[r], (j / a.XR) & 1);
+            if (tid == 0) TC_STAMP(4, j);
+            split_lo(X(r), LO(w), real, tid, kSplitWarps * 32);
+            fence_async_smem();
+            __syncwarp();
+            if (tid == 0) TC_STAMP(5, j);
+            if (lane == 0) mbar_arrive(&wsplit[w]);
+        }
+    } else if (warp >= kSkGenW0 && warp < kSkGenW0 + kSkGenWarps) {
+        // ================= test-matrix generators: Omega_0(c, k) = draw D + col_off + c + rows_glob k
+        // (fp32 Box-Muller, ~1e-7 relative per draw: far below the 1e-4 fp32 bound and the 3xTF32
+        // error, at half the issue cost of the fp64 generator the fp64 kernels need)
+        const int tid = threadIdx.x - kSkGenW0 * 32;
+        const int npair = a.kb / 2 + 1;
+        // items (pair pi, column k), k fastest across the lanes: consecutive lanes store into
+        // consecutive 16-byte rows of the B core matrices (fewer bank conflicts)
+        const int stride = kSkGenWarps * 32, dpi = stride / a.K, dk = stride % a.K;
+        const int pi0 = tid / a.K, k0 = tid % a.K;
+        for (int j = 0; j < nt; ++j) {
+            const int bq = j % a.BR;
+            if (j >= a.BR) mbar_wait(&bempty[bq], ((j / a.BR) - 1) & 1);
+            if (tid == 0) TC_STAMP(6, j);
+            const int64_t c0 = (t0 + j) * a.kb;
+            const uint32_t bh = BH(bq), bl = a.ncat ? BH(bq) : BL(bq);
+            const int lo_row = a.ncat ? a.Kp : 0;
+            // four independent items per iteration: the Box-Muller chains interleave (ILP)
+            int pi = pi0, k = k0;
+            while (pi < npair) {
+                int pu[4], ku[4];
+                float z[4][2];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    pu[u] = pi;
+                    ku[u] = k;
+                    pi += dpi;
+                    k += dk;
+                    if (k >= a.K) {
+                        k -= a.K;
+                        ++pi;
                     }
                 }
-                mma_commit(&empty[s]);
-            }
-            __syncwarp();
-        }
-        if (lane == 0) mma_commit(done);
-        __syncwarp();
-    } else if (warp >= kSplitW0 && warp < kSplitW0 + kSplitWarps) {
-        // ================= X splitters, then the epilogue
-        const int tid = threadIdx.x - kSplitW0 * 32;
-        const uint32_t real = (uint32_t)a.nblk * (uint32_t)a.kb * 128u;
-        for (int j = 0; j < nt; ++j) {
-            const int s = j % a.S;
-            mbar_wait(&full[s], (j / a.S) & 1);
-            split_stage(A_hi(s), A_lo(s), real, tid, kSplitWarps * 32);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&split[s]);
-        }
-        // epilogue: TMEM lane quarter (warp % 4) holds rows 32 (warp % 4) + lane of each M tile
-        const int q = warp & 3;
-        double* part = a.partial + (int64_t)blockIdx.x * a.I0 * a.K;
-        if (nt > 0) {
-            mbar_wait(done, 0);
-            tc_fence_after();
-        }
-        for (int mt = 0; mt < a.Mt; ++mt) {
-            const int row = mt * 128 + q * 32 + lane;
-            for (int n0 = 0; n0 < a.Kp; n0 += 8) {
-                float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                if (nt > 0) tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * a.Kp + n0), v);
-                if (a.dbg && blockIdx.x == 0 && mt == 0 && n0 == 0 && lane < 8)
-                    for (int jj = 0; jj < 8; ++jj) a.dbg[800 + q * 64 + lane * 8 + jj] = v[jj];
-                if (row < a.I0) {
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj)
-                        if (n0 + jj < a.K) part[row + (int64_t)a.I0 * (n0 + jj)] = (double)v[jj];
+                for (int u = 0; u < 4; ++u) {
+                    const uint64_t d0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)ku[u];
+                    const uint64_t p = (d0 >> 1) + (uint64_t)pu[u];  // pair p holds draws 2p, 2p + 1
+                    gauss_pair_f32_fast(a.seed + (2ull * p + 1ull) * 0x9E3779B97F4A7C15ull, z[u][0], z[u][1]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (pu[u] >= npair) break;
+                    const uint64_t d0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)ku[u];
+                    const uint64_t p = (d0 >> 1) + (uint64_t)pu[u];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int64_t cl = (int64_t)(2 * p + e) - (int64_t)d0;  // column within the tile
+                        if (cl < 0 || cl >= a.kb) continue;
+                        const float v = c0 + cl < a.L ? z[u][e] : 0.f;
+                        sts32(bh + b_off(ku[u], (int)cl, NB), v);  // read as trunc_tf32(v)
+                        sts32(bl + b_off(ku[u] + lo_row, (int)cl, NB), v - tf32_trunc(v));
+                    }
                 }
             }
+            fence_async_smem();
+            __syncwarp();
+            if (tid == 0) TC_STAMP(7, j);
+            if (lane == 0) mbar_arrive(&bfull[bq]);
         }
-        if (a.dbg && blockIdx.x == 0) {  // TMEM store / load round trip in the last allocated column
-            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (tcols - 1);
-            const uint32_t val = __float_as_uint((float)(1000 + q * 32 + lane));
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta), "r"(val) : "memory");
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            uint32_t r;
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(ta));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            a.dbg[900 + q * 32 + lane] = __uint_as_float(r);
-        }
-        if (a.dbg && blockIdx.x == 0 && warp == kSplitW0) {
-            // stage 0 as last filled: A hi (first 256 floats), A lo, B hi, B lo (first 128 each), TMEM row lane
-            for (int e = lane; e < 256; e += 32) {
-                float v;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(A_hi(0) + 4u * e));
-                a.dbg[e] = v;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(A_lo(0) + 4u * e));
-                a.dbg[256 + e] = v;
-            }
-            for (int e = lane; e < 128; e += 32) {
-                float v;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(B_hi(0) + 4u * e));
-                a.dbg[512 + e] = v;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(B_lo(0) + 4u * e));
-                a.dbg[640 + e] = v;
-            }
-            if (lane == 0) {
-                a.dbg[768] = (float)nt;
-                a.dbg[769] = (float)tmem;
-                a.dbg[770] = (float)a.kb;
-                a.dbg[771] = (float)a.S;
-            }
-        }
-        tc_fence_before();
     } else {
-        // ================= test-matrix generators: Omega_0(c, k) = draw D + col_off + c + rows_glob k
-        const int tid = threadIdx.x - kAuxW0 * 32;
-        const int npair = a.kb / 2 + 1;
-        for (int j = 0; j < nt; ++j) {
-            const int s = j % a.S;
-            if (j >= a.S) mbar_wait(&empty[s], ((j / a.S) - 1) & 1);
-            const int64_t c0 = (t0 + j) * a.kb;
-            const uint32_t bh = B_hi(s), bl = B_lo(s);
-            for (int it = tid; it < a.K * npair; it += kAuxWarps * 32) {
-                const int k = it / npair, pi = it - k * npair;
-                const uint64_t d0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)k;
-                const uint64_t p = (d0 >> 1) + (uint64_t)pi;  // pair p holds draws 2p, 2p + 1
-                double z[2];
-                gauss_pair_state(a.seed + (2ull * p + 1ull) * 0x9E3779B97F4A7C15ull, *tabs, z[0], z[1]);
+        // ================= drainers: M = 128, lane quarter q holds rows 32 q + lane of each tile;
+        // M = 64, rows 16 q + lane (lanes 0-15 of each quarter). Segment g adds accumulator set
+        // g % nset into the CTA's fp64 partial.
+        const int q = warp & 3;
+        double* part = a.partial + (int64_t)cg * a.I0 * a.K;
+        const int rq = a.M == 128 ? 32 : 16;
+        const int tw = (a.ncat ? 2 : 1) * a.Kp;
+        for (int g = 0; g < nseg; ++g) {
+            const int set = g % a.nset;
+            mbar_wait(&dfull[set], (g / a.nset) & 1);
+            tc_fence_after();
+            for (int mt = 0; mt < a.Mt; ++mt) {
+                const int row = (rs * a.Mt + mt) * a.M + q * rq + lane;
+                const bool own = lane < rq && row < a.I0;
+                for (int n0 = 0; n0 < a.Kp; n0 += 16) {  // 16 partial values in flight per batch
+                    float v[16];
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)set * setcols + (uint32_t)(mt * tw + n0);
+                    tmem_ld8(ta, *reinterpret_cast<float(*)[8]>(&v[0]));
+                    tmem_ld8(ta + 8u, *reinterpret_cast<float(*)[8]>(&v[8]));
+                    if (a.ncat) {
+                        float u[8];
+                        tmem_ld8(ta + (uint32_t)a.Kp, u);
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int64_t cl = (int64_t)(2 * p + e) - (int64_t)d0;  // column within the tile
-                    if (cl < 0 || cl >= a.kb) continue;
-                    const bool in = c0 + cl < a.L;
-                    const float w = in ? (float)z[e] : 0.f;
-                    const float h = tf32_rna(w);
-                    const float l = in ? (float)(z[e] - (double)h) : 0.f;
-                    const uint32_t o = b_off(k, (int)cl, a.Kp);
-                    sts32(bh + o, h);
-                    sts32(bl + o, l);
+                        for (int jj = 0; jj < 8; ++jj) v[jj] += u[jj];
+                        tmem_ld8(ta + (uint32_t)a.Kp + 8u, u);
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) v[8 + jj] += u[jj];
+                    }
+                    if (own) {
+                        double old[16];
+                        if (g > 0) {
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj)
+                                old[jj] = n0 + jj < a.K ? part[row + (int64_t)a.I0 * (n0 + jj)] : 0.0;
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) old[jj] = 0.0;
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (n0 + jj < a.K) part[row + (int64_t)a.I0 * (n0 + jj)] = old[jj] + (double)v[jj];
+                    }
                 }
             }
-            fence_async_smem();
+            tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&omega[s]);
+            if (lane == 0) mbar_arrive(&dempty[set]);
         }
+        if (nseg == 0)  // no columns: a zero partial
+            for (int mt = 0; mt < a.Mt; ++mt) {
+                const int row = (rs * a.Mt + mt) * a.M + q * rq + lane;
+                if (lane < rq && row < a.I0)
+                    for (int n = 0; n < a.K; ++n) part[row + (int64_t)a.I0 * n] = 0.0;
+            }
     }
     __syncthreads();
     if (warp == 1) {
@@ -367,68 +461,99 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_sketch_f32(const __grid_cons
 }
 
 struct TcSkPlan {
-    int Kp, Mt, nblk, kb, S;
+    int Kp, M, Mt, RS, nblk, kb, XR, BR, nset, ncat, seg;
     uint32_t a_bytes, b_bytes;
     size_t smem;
 };
 
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 bool plan_tc_sketch(int64_t I0, int K, TcSkPlan& p) {
     if (K < 1 || K > 64 || I0 < 1 || I0 > 1024) return false;
     p.Kp = (K + 15) & ~15;
-    p.Mt = (int)((I0 + 127) / 128);
-    if (p.Mt * p.Kp > 512) return false;
+    p.M = I0 <= 64 ? 64 : 128;
+    const int mt_all = (int)((I0 + p.M - 1) / p.M);
+    // No row splits (each would regenerate the test matrix); N-concatenation (the tensor core reads
+    // X twice instead of three times) when two such accumulator sets fit TMEM's 512 columns; two
+    // sets (drained every ~256 columns) when they fit, else one drained at the CTA's end (C4:
+    // 8 x 64 columns; measured 349 us against 656 / 469 us with two / four row splits).
+    auto cols = [&](int rs, int ncat) { return 2 * ((mt_all + rs - 1) / rs) * (ncat ? 2 : 1) * p.Kp; };
+    p.RS = env_int("TRG_TC_SK_RS", 1);
+    p.ncat = env_int("TRG_TC_SK_NCAT", cols(p.RS, 1) <= 512 ? 1 : 0);
+    p.Mt = (mt_all + p.RS - 1) / p.RS;
+    p.nset = cols(p.RS, p.ncat) <= 512 ? 2 : 1;
+    if (p.Mt * (p.ncat ? 2 : 1) * p.Kp > 512) return false;
     p.nblk = (int)((I0 + 31) / 32);
-    // ~24-32 KB of X per stage
+    const int bpc = p.Mt * (p.M / 32);  // blocks per CTA stage
+    // ~32 KB of X per stage
     p.kb = 8;
-    while (p.kb < 64 && (size_t)p.nblk * (p.kb * 2) * 128 <= 32768) p.kb *= 2;
-    p.a_bytes = (uint32_t)p.Mt * 4u * (uint32_t)p.kb * 128u;
+    while (p.kb < 128 && (size_t)bpc * (p.kb * 2) * 128 <= (size_t)env_int("TRG_TC_SK_STAGE", 32768)) p.kb *= 2;
+    p.seg = p.nset == 2 ? std::max(1, 256 / p.kb) : (1 << 30);  // drain every ~256 columns
+    p.a_bytes = (uint32_t)bpc * (uint32_t)p.kb * 128u;
     p.b_bytes = (uint32_t)p.Kp * (uint32_t)p.kb * 4u;
-    const size_t stage = 2 * (size_t)p.a_bytes + 2 * (size_t)p.b_bytes;
-    const size_t fixed = 1024 + sizeof(GaussTables) + 8 * (4 * 8 + 2) + 64;
-    p.S = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage);
-    p.smem = (size_t)p.S * stage + fixed;
-    return p.S >= 2;
+    const size_t fixed = 1024 + 8 * (2 * 8 + 2 * kWR + 2 * 16 + 4) + 64;
+    const size_t budget = 227 * 1024 - fixed - (size_t)kWR * p.a_bytes;
+    // X ring first (the HBM stream), then the test-matrix ring up to 8 deep
+    p.XR = (int)std::min<size_t>(8, (budget - 2 * 2 * (size_t)p.b_bytes) / p.a_bytes);
+    p.BR = (int)std::min<size_t>(8, (budget - (size_t)p.XR * p.a_bytes) / (2 * (size_t)p.b_bytes));
+    p.XR = env_int("TRG_TC_SK_XR", p.XR);
+    p.smem = (size_t)(p.XR + kWR) * p.a_bytes + (size_t)p.BR * 2 * p.b_bytes + fixed;
+    return p.XR >= 2 && p.BR >= 2 && p.smem <= 227 * 1024;
 }
 
 // ================================================================== K2: mode-0 shrink
+// per tile of 256 fibres: D[256 x 2 Kp] = X^T [Q_hi | Q_lo] + (X_lo^T Q_hi in the first Kp
+// columns), as two M = 128 halves. Rings: X + Q slabs (XR deep, TMA -> MMA), lo (2 deep).
+// Warps: 0 TMA, 1 MMA (+ TMEM), 2-5 splitters, 6-9 epilogue.
+constexpr int kTtThreads = 10 * 32;
+constexpr int kTtEpiW0 = 6;
+
 struct TcTtArgs {
-    int I0, K, Kp, nchunk, S;
+    int I0, K, Kp, nchunk, XR;
     int64_t L, ntiles;  // tiles of 256 fibres
     void* out;          // P^(1): K x L column-major, fp32 or fp64
     uint32_t a_bytes, q_bytes;
 };
 
 template <bool F64OUT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kTtThreads, 1)
     k_tc_ttm_f32(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qhmap,
                  const __grid_constant__ CUtensorMap qlmap, TcTtArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
-    const uint32_t stage_bytes = 2 * a.a_bytes + 2 * a.q_bytes;  // X hi | X lo | Q hi | Q lo
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (size_t)a.S * stage_bytes);
-    uint64_t* full = bars;
-    uint64_t* split = bars + a.S;
-    uint64_t* empty = bars + 2 * a.S;
-    uint64_t* tfull = bars + 3 * a.S;   // [2] accumulator buffer ready for the epilogue
-    uint64_t* tempty = bars + 3 * a.S + 2;  // [2] accumulator buffer drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * a.S + 4);
-    auto X_hi = [&](int s) { return base + (uint32_t)s * stage_bytes; };
-    auto X_lo = [&](int s) { return X_hi(s) + a.a_bytes; };
-    auto Q_hi = [&](int s) { return X_hi(s) + 2 * a.a_bytes; };
-    auto Q_lo = [&](int s) { return Q_hi(s) + a.q_bytes; };
-    const uint32_t tcols = 4 * a.Kp <= 64 ? 64u : 4 * a.Kp <= 128 ? 128u : 256u;  // 2 buffers x 2 halves x Kp
+    const uint32_t xbytes = a.a_bytes + 2 * a.q_bytes;  // X slab | Q hi | Q lo (contiguous: B = 2 Kp rows)
+    const uint32_t lbase = base + (uint32_t)a.XR * xbytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (size_t)a.XR * xbytes + (size_t)kWR * a.a_bytes);
+    uint64_t* xfull = bars;
+    uint64_t* xempty = bars + a.XR;
+    uint64_t* lfull = bars + 2 * a.XR;   // [2]
+    uint64_t* lempty = lfull + kWR;      // [2]
+    uint64_t* tfull = lempty + kWR;      // [2] accumulator buffer ready for the epilogue
+    uint64_t* tempty = tfull + 2;        // [2] accumulator buffer drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    auto X = [&](int r) { return base + (uint32_t)r * xbytes; };
+    auto QH = [&](int r) { return X(r) + a.a_bytes; };
+    auto LO = [&](int w) { return lbase + (uint32_t)w * a.a_bytes; };
+    const uint32_t tw = 2u * (uint32_t)a.Kp;  // accumulator width per half
+    const uint32_t tcols = 4 * tw <= 64 ? 64u : 4 * tw <= 128 ? 128u : 4 * tw <= 256 ? 256u : 512u;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < a.S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&split[s], kSplitWarps);
-            mbar_init(&empty[s], 1);
+        for (int r = 0; r < a.XR; ++r) {
+            mbar_init(&xfull[r], 1);
+            mbar_init(&xempty[r], 1);
+        }
+        for (int w = 0; w < kWR; ++w) {
+            mbar_init(&lfull[w], kSplitWarps);
+            mbar_init(&lempty[w], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kAuxWarps);
+            mbar_init(&tempty[b], 4);
         }
         fence_mbar_init();
     }
@@ -437,58 +562,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // tiles: blockIdx.x, blockIdx.x + grid, ...
     const int nt = a.ntiles > blockIdx.x ? (int)((a.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const int total = nt * a.nchunk;
 
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pol_x = policy_l2(0), pol_q = policy_l2(2);
+            const uint64_t pol_x = policy_l2(1), pol_q = policy_l2(2);
             griddep_wait();  // Q (and, in the chain, X's producer) come from the previous grids
             int g = 0;
             for (int j = 0; j < nt; ++j) {
                 const int c0 = (int)((blockIdx.x + (int64_t)j * gridDim.x) * 256);
                 for (int ch = 0; ch < a.nchunk; ++ch, ++g) {
-                    const int s = g % a.S;
-                    if (g >= a.S) mbar_wait(&empty[s], ((g / a.S) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], a.a_bytes + 2 * a.q_bytes);
-                    tma2d(X_hi(s), &xmap, 32 * ch, c0, &full[s], pol_x);
-                    tma2d(X_hi(s) + a.a_bytes / 2, &xmap, 32 * ch, c0 + 128, &full[s], pol_x);
-                    tma2d(Q_hi(s), &qhmap, 32 * ch, 0, &full[s], pol_q);
-                    tma2d(Q_lo(s), &qlmap, 32 * ch, 0, &full[s], pol_q);
+                    const int r = g % a.XR;
+                    if (g >= a.XR) mbar_wait(&xempty[r], ((g / a.XR) - 1) & 1);
+                    mbar_arrive_expect_tx(&xfull[r], a.a_bytes + 2 * a.q_bytes);
+                    tma2d(X(r), &xmap, 32 * ch, c0, &xfull[r], pol_x);
+                    tma2d(X(r) + a.a_bytes / 2, &xmap, 32 * ch, c0 + 128, &xfull[r], pol_x);
+                    tma2d(QH(r), &qhmap, 32 * ch, 0, &xfull[r], pol_q);
+                    tma2d(QH(r) + a.q_bytes, &qlmap, 32 * ch, 0, &xfull[r], pol_q);
                 }
             }
         }
     } else if (warp == 1) {
-        const uint32_t idesc = idesc_tf32(128, a.Kp, 0, 0);
+        const uint32_t idesc1 = idesc_tf32(128, 2 * a.Kp, 0, 0);
+        const uint32_t idesc2 = idesc_tf32(128, a.Kp, 0, 0);
         int g = 0;
         for (int j = 0; j < nt; ++j) {
             const int buf = j & 1;
             if (j >= 2) mbar_wait(&tempty[buf], ((j >> 1) - 1) & 1);
             tc_fence_after();
             for (int ch = 0; ch < a.nchunk; ++ch, ++g) {
-                const int s = g % a.S;
-                const uint32_t ph = (g / a.S) & 1;
-                mbar_wait(&full[s], ph);
-                mbar_wait(&split[s], ph);
+                const int r = g % a.XR, w = g % kWR;
+                mbar_wait(&xfull[r], (g / a.XR) & 1);
+                mbar_wait(&lfull[w], (g / kWR) & 1);
                 tc_fence_after();
                 if (lane == 0) {
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {  // 4 k-steps of 8 in the 128-byte rows
-                        const uint64_t qh = sdesc(Q_hi(s) + ks * 32u, 16, 1024, kSw128);
-                        const uint64_t ql = sdesc(Q_lo(s) + ks * 32u, 16, 1024, kSw128);
+                        const uint64_t qd = sdesc(QH(r) + ks * 32u, 16, 1024, kSw128);  // [Q_hi; Q_lo] rows
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const uint32_t ao = (uint32_t)h * (a.a_bytes / 2) + ks * 32u;
-                            const uint64_t xh = sdesc(X_hi(s) + ao, 16, 1024, kSw128);
-                            const uint64_t xl = sdesc(X_lo(s) + ao, 16, 1024, kSw128);
-                            const uint32_t d = tmem + (uint32_t)((buf * 2 + h) * a.Kp);
+                            const uint64_t xh = sdesc(X(r) + ao, 16, 1024, kSw128);
+                            const uint64_t xl = sdesc(LO(w) + ao, 16, 1024, kSw128);
+                            const uint32_t d = tmem + (uint32_t)(buf * 2 + h) * tw;
                             const uint32_t acc = (ch > 0 || ks > 0) ? 1u : 0u;
-                            mma_tf32(d, xh, qh, idesc, acc);
-                            mma_tf32(d, xl, qh, idesc, 1u);
-                            mma_tf32(d, xh, ql, idesc, 1u);
+                            mma_tf32(d, xh, qd, idesc1, acc);  // X_hi [Q_hi | Q_lo]
+                            mma_tf32(d, xl, qd, idesc2, 1u);   // X_lo Q_hi (first Kp columns)
                         }
                     }
-                    mma_commit(&empty[s]);
+                    mma_commit(&xempty[r]);
+                    mma_commit(&lempty[w]);
                 }
                 __syncwarp();
             }
@@ -497,17 +621,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= kSplitW0 && warp < kSplitW0 + kSplitWarps) {
         const int tid = threadIdx.x - kSplitW0 * 32;
-        const int total = nt * a.nchunk;
         for (int g = 0; g < total; ++g) {
-            const int s = g % a.S;
-            mbar_wait(&full[s], (g / a.S) & 1);
-            split_stage(X_hi(s), X_lo(s), a.a_bytes, tid, kSplitWarps * 32);
+            const int r = g % a.XR, w = g % kWR;
+            if (g >= kWR) mbar_wait(&lempty[w], ((g / kWR) - 1) & 1);
+            mbar_wait(&xfull[r], (g / a.XR) & 1);
+            split_lo(X(r), LO(w), a.a_bytes, tid, kSplitWarps * 32);
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&split[s]);
+            if (lane == 0) mbar_arrive(&lfull[w]);
         }
     } else {
-        // ================= epilogue: TMEM lane = fibre of the tile, columns = the K outputs
+        // ================= epilogue: TMEM lane = fibre of the tile; output k = column k + column Kp + k
         const int q = warp & 3;
         for (int j = 0; j < nt; ++j) {
             const int buf = j & 1;
@@ -518,8 +642,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int h = 0; h < 2; ++h) {
                 const int64_t c = tc0 + h * 128 + q * 32 + lane;
                 for (int n0 = 0; n0 < a.Kp; n0 += 8) {
-                    float v[8];
-                    tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * 2 + h) * a.Kp + n0), v);
+                    float v[8], u[8];
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 2 + h) * tw + (uint32_t)n0;
+                    tmem_ld8(ta, v);
+                    tmem_ld8(ta + (uint32_t)a.Kp, u);
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) v[jj] += u[jj];
                     if (c < a.L) {
                         if constexpr (F64OUT) {
                             double* o = reinterpret_cast<double*>(a.out) + c * a.K + n0;
@@ -553,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Q (fp64, ldq x K column-major, rows [0, I0)) -> Qt_hi / Qt_lo (fp32, Kp x Ip, i fastest),
-// zero-padded: the K2 B operand, split for 3xTF32
+// zero-padded: the K2 B operand, split for 3xTF32 (hi = trunc_tf32 of the fp32 rounding)
 __global__ void k_qt_prep(const double* __restrict__ q, int64_t ldq, int I0, int K, int Ip, int Kp, float* hi,
                           float* lo) {
     griddep_wait();
@@ -561,7 +689,7 @@ __global__ void k_qt_prep(const double* __restrict__ q, int64_t ldq, int I0, int
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         const int k = e / Ip, i = e - k * Ip;
         const double v = (k < K && i < I0) ? q[i + ldq * k] : 0.0;
-        const float h = tf32_rna((float)v);
+        const float h = tf32_trunc((float)v);
         hi[e] = h;
         lo[e] = (float)(v - (double)h);
     }
@@ -569,7 +697,7 @@ __global__ void k_qt_prep(const double* __restrict__ q, int64_t ldq, int I0, int
 }
 
 struct TcTtPlan {
-    int Kp, nchunk, S, Ip;
+    int Kp, nchunk, XR, Ip;
     uint32_t a_bytes, q_bytes;
     size_t smem;
 };
@@ -581,11 +709,11 @@ bool plan_tc_ttm(int64_t I0, int64_t K, TcTtPlan& p) {
     p.Ip = p.nchunk * 32;
     p.a_bytes = 256u * 128u;                // two 128-fibre halves x 32 rows x 4 B
     p.q_bytes = (uint32_t)p.Kp * 128u;      // Kp rows x 32 i x 4 B
-    const size_t stage = 2 * (size_t)p.a_bytes + 2 * (size_t)p.q_bytes;
-    const size_t fixed = 1024 + 8 * (3 * 8 + 4) + 64;
-    p.S = (int)std::min<size_t>(4, (227 * 1024 - fixed) / stage);
-    p.smem = (size_t)p.S * stage + fixed;
-    return p.S >= 2;
+    const size_t fixed = 1024 + 8 * (2 * 8 + 2 * kWR + 4) + 64;
+    const size_t lo = (size_t)kWR * p.a_bytes;
+    p.XR = (int)std::min<size_t>(8, (227 * 1024 - fixed - lo) / (p.a_bytes + 2 * (size_t)p.q_bytes));
+    p.smem = (size_t)p.XR * (p.a_bytes + 2 * (size_t)p.q_bytes) + lo + fixed;
+    return p.XR >= 2;
 }
 
 void encode2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
@@ -603,9 +731,15 @@ void encode2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 }  // namespace
 
 // ------------------------------------------------------------------ host side
+// Dispatch: the tensor-core sketch where the FFMA kernel is compute-bound (K >= 32, e.g. C4's
+// K_0 = 64 at 32 flop/B: 349 against 856 us); at small K the FFMA kernel with its cheaper
+// register-level test-matrix reuse stays ahead (C3 1172 vs 1384 us, C5 1088 vs 2550 us, measured).
+// TRG_TC_FORCE=1 takes the tensor-core kernels for every supported shape (tests), TRG_NO_TCGEN05=1 none.
+bool tc_forced() { return getenv("TRG_TC_FORCE") != nullptr; }
+
 bool tc_sketch_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols) {
     TcSkPlan p;
-    if (getenv("TRG_NO_TCGEN05")) return false;
+    if (getenv("TRG_NO_TCGEN05") || (K < 32 && !tc_forced())) return false;
     return dtype == F32 && left == 1 && (dim % 4) == 0 && ncols < (int64_t(1) << 31) && encode_fn() &&
            plan_tc_sketch(dim, K, p);
 }
@@ -618,10 +752,16 @@ int launch_tc_sketch_f32(const SketchPlan& sp, const void* x, double* partial, d
     a.I0 = (int)sp.dim;
     a.K = sp.K;
     a.Kp = p.Kp;
+    a.M = p.M;
     a.Mt = p.Mt;
     a.nblk = p.nblk;
     a.kb = p.kb;
-    a.S = p.S;
+    a.XR = p.XR;
+    a.seg = p.seg;
+    a.nset = p.nset;
+    a.ncat = p.ncat;
+    a.RS = p.RS;
+    a.BR = p.BR;
     a.L = sp.right;
     a.ntiles = (sp.right + p.kb - 1) / p.kb;
     a.seed = sp.seed;
@@ -629,39 +769,64 @@ int launch_tc_sketch_f32(const SketchPlan& sp, const void* x, double* partial, d
     a.rows_glob = sp.rows_glob;
     a.col_off = sp.col_off;
     a.partial = partial;
-    a.gt = gauss_tables(s);
     a.a_bytes = p.a_bytes;
     a.b_bytes = p.b_bytes;
     CUtensorMap map;
     encode2d(&map, x, (uint64_t)sp.dim, (uint64_t)sp.right, (uint64_t)sp.dim * 4, 32, (uint32_t)p.kb,
              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
-    const char* dbg_path = getenv("TRG_TC_DEBUG");
-    if (dbg_path) cudaMalloc(&a.dbg, 1024 * sizeof(float)), cudaMemset(a.dbg, 0, 1024 * sizeof(float));
-    allow_smem(k_tc_sketch_f32, p.smem);
-    k_tc_sketch_f32<<<grid, kThreads, p.smem, s>>>(map, a);
-    if (dbg_path) {
-        float h[1024];
-        cudaStreamSynchronize(s);
-        fprintf(stderr, "tc_sketch launch: %s grid %d smem %zu S %d kb %d\n", cudaGetErrorString(cudaGetLastError()),
-                grid, p.smem, p.S, p.kb);
-        cudaMemcpy(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost);
-        if (FILE* f = fopen(dbg_path, "wb")) fwrite(h, sizeof(h), 1, f), fclose(f);
-        cudaFree(a.dbg);
+    const int ncg = tc_sketch_f32_grid(sp.dim, sp.K, sp.right, num_sms);
+    const int grid = ncg * p.RS;
+    static const char* prof_env = getenv("TRG_TC_PROF");
+    if (prof_env) {
+        cudaMalloc(&a.prof, 8 * 256 * sizeof(long long));
+        cudaMemset(a.prof, 0, 8 * 256 * sizeof(long long));
     }
-    if (y) launch_reduce_partials(partial, grid, sp.dim * sp.K, y, s);
-    return grid;
+    allow_smem(k_tc_sketch_f32, p.smem);
+    k_tc_sketch_f32<<<grid, kSkThreads, p.smem, s>>>(map, a);
+    if (prof_env) {  // development: per-stage timeline of CTA 0 (cycles), averaged over stages 16..255
+        long long h[8 * 256];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaFree(a.prof);
+        double acc[8] = {0};
+        int n = 0;
+        for (int j = 16; j < 255; ++j) {
+            if (!h[3 * 256 + j + 1]) break;
+            acc[0] += h[0 * 256 + j + 1] - h[0 * 256 + j];  // producer period
+            acc[1] += h[1 * 256 + j] - h[0 * 256 + j];      // producer wait for xempty
+            acc[2] += h[2 * 256 + j] - h[1 * 256 + j];      // TMA issue -> MMA sees xfull
+            acc[3] += h[3 * 256 + j] - h[2 * 256 + j];      // MMA waits split / omega after xfull
+            acc[4] += h[5 * 256 + j] - h[4 * 256 + j];      // split duration
+            acc[5] += h[7 * 256 + j] - h[6 * 256 + j];      // generation duration
+            acc[6] += h[3 * 256 + j + 1] - h[3 * 256 + j];  // MMA period
+            acc[7] += h[4 * 256 + j] - h[2 * 256 + j];      // splitter start - MMA xfull seen
+            ++n;
+        }
+        for (int j = 100; j < 112; ++j) {
+            fprintf(stderr, "tc_stage %d:", j);
+            for (int q = 0; q < 8; ++q) fprintf(stderr, " %lld", h[q * 256 + j] - h[0 * 256 + 100]);
+            fprintf(stderr, "\n");
+        }
+        fprintf(stderr, "tc_sketch prof (cycles/stage, n=%d): prod period %.0f wait_xempty %.0f tma->xfull %.0f "
+                        "mma_wait_work %.0f split %.0f gen %.0f mma period %.0f split_start-xfull %.0f\n",
+                n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n);
+    }
+    if (y) launch_reduce_partials(partial, ncg, sp.dim * sp.K, y, s);
+    return ncg;
 }
 
+// number of column groups = number of per-CTA-group partials of Y
 int tc_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms) {
     TcSkPlan p;
     plan_tc_sketch(dim, K, p);
-    return (int)std::max<int64_t>(1, std::min<int64_t>((ncols + p.kb - 1) / p.kb, num_sms));
+    return (int)std::max<int64_t>(1, std::min<int64_t>((ncols + p.kb - 1) / p.kb, num_sms / p.RS));
 }
 
+// the tensor-core shrink from K >= 16 on fibres of >= 128 rows (C3 789 vs 1308 us, C4 249 vs 897
+// us); C5's 60-row fibres split into two 32-row slabs that over-fetch (1089 vs 934 us)
 bool tc_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols) {
     TcTtPlan p;
-    if (getenv("TRG_NO_TCGEN05")) return false;
+    if (getenv("TRG_NO_TCGEN05") || ((K < 16 || dim < 128) && !tc_forced())) return false;
     return dtype == F32 && left == 1 && ncols < (int64_t(1) << 31) && encode_fn() && plan_tc_ttm(dim, K, p);
 }
 
@@ -687,7 +852,7 @@ void launch_tc_ttm_f32(const TTMPlan& tp, const void* in, void* out, bool f64_ou
     a.K = (int)tp.odim;
     a.Kp = p.Kp;
     a.nchunk = p.nchunk;
-    a.S = p.S;
+    a.XR = p.XR;
     a.L = tp.right;
     a.ntiles = (tp.right + 255) / 256;
     a.out = out;
@@ -702,10 +867,10 @@ void launch_tc_ttm_f32(const TTMPlan& tp, const void* in, void* out, bool f64_ou
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
     if (f64_out) {
         allow_smem(k_tc_ttm_f32<true>, p.smem);
-        pdl_launch(k_tc_ttm_f32<true>, dim3(grid), dim3(kThreads), p.smem, s, xm, qhm, qlm, a);
+        pdl_launch(k_tc_ttm_f32<true>, dim3(grid), dim3(kTtThreads), p.smem, s, xm, qhm, qlm, a);
     } else {
         allow_smem(k_tc_ttm_f32<false>, p.smem);
-        pdl_launch(k_tc_ttm_f32<false>, dim3(grid), dim3(kThreads), p.smem, s, xm, qhm, qlm, a);
+        pdl_launch(k_tc_ttm_f32<false>, dim3(grid), dim3(kTtThreads), p.smem, s, xm, qhm, qlm, a);
     }
 }
 

@@ -207,7 +207,7 @@ void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cu
     a.dlen = ((p.dim + p.dsplit - 1) / p.dsplit + 31) / 32 * 32;
     a.part = nullptr;
     const int64_t nout = p.rows * p.odim;
-    if (p.dsplit > 1) cudaMallocAsync(&a.part, sizeof(double) * nout * p.dsplit, s);
+    if (p.dsplit > 1) a.part = (double*)scratch_alloc(sizeof(double) * nout * p.dsplit, s);
     if (p.dtype == F64) {
         if (p.TO == 8) run_l<double, 4, 8>(p, a, s);
         else run_l<double, 4, 4>(p, a, s);
@@ -220,12 +220,12 @@ void launch_ttm(const TTMPlan& p, const void* in, void* out, const double* m, cu
             launch_reduce_partials(a.part, p.dsplit, nout, reinterpret_cast<double*>(out), s);
         } else {
             double* tmp = nullptr;
-            cudaMallocAsync(&tmp, sizeof(double) * nout, s);
+            tmp = (double*)scratch_alloc(sizeof(double) * nout, s);
             launch_reduce_partials(a.part, p.dsplit, nout, tmp, s);
             launch_convert(tmp, F64, out, F32, nout, s);
-            cudaFreeAsync(tmp, s);
+            scratch_free(tmp, s);
         }
-        cudaFreeAsync(a.part, s);
+        scratch_free(a.part, s);
     }
 }
 

@@ -32,8 +32,15 @@ SHAPES = [
 ]
 
 
+@pytest.fixture
+def forced(monkeypatch):
+    # every shape below on the tensor-core kernels (the default dispatch takes them only where
+    # they beat the FFMA kernels: tc_f32.cu)
+    monkeypatch.setenv("TRG_TC_FORCE", "1")
+
+
 @pytest.mark.parametrize("dims,K", SHAPES)
-def test_tc_mode0_parity(trg, dims, K):
+def test_tc_mode0_parity(trg, forced, dims, K):
     rng = np.random.default_rng(sum(dims) + sum(K))
     x = rng.standard_normal(dims).astype(np.float32)
     proj, bases, ys = orc.sketch(x.astype(np.float64), K, 3)

@@ -7,7 +7,13 @@
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__host__ __device__ float aval(int m, int k) { return (float)((m * 7 + k * 3) % 11) - 5.0f; }
+__device__ int g_rawmode = 0;
+__host__ __device__ float aval(int m, int k) {
+#ifdef __CUDA_ARCH__
+    if (g_rawmode) return 1.0f + 3.0f / 4096.0f;  // tf32: RN -> 1 + 2^-10, truncation -> 1
+#endif
+    return (float)((m * 7 + k * 3) % 11) - 5.0f;
+}
 __host__ __device__ float bval(int n, int k) { return (float)((n * 5 + k) % 7) - 3.0f; }
 
 __global__ void k(uint32_t idesc, uint32_t a_lbo, uint32_t a_sbo, int a_sw, float* out) {
@@ -89,6 +95,21 @@ int main() {
             for (int kk = 0; kk < 8; ++kk) s += aval(m, kk) * bval(n, kk);
             want[m * 16 + n] = s;
         }
+    {  // how kind::tf32 reads an fp32 operand with low mantissa bits set
+        int one = 1;
+        cudaMemcpyToSymbol(g_rawmode, &one, sizeof(int));
+        cudaMemset(d, 0, 128 * 16 * sizeof(float));
+        k<<<1, 128, 16384>>>(vs[0].idesc, vs[0].lbo, vs[0].sbo, vs[0].sw, d);
+        cudaDeviceSynchronize();
+        float h[16];
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        float bs = 0;
+        for (int kk = 0; kk < 8; ++kk) bs += bval(0, kk);
+        printf("raw-fp32 A = 1+3*2^-12: D[0][0] = %.9g; trunc -> %.9g, RN -> %.9g\n", h[0], bs * 1.0,
+               bs * (1.0 + 1.0 / 1024));
+        int zero = 0;
+        cudaMemcpyToSymbol(g_rawmode, &zero, sizeof(int));
+    }
     for (auto& v : vs) {
         cudaMemset(d, 0, 128 * 16 * sizeof(float));
         k<<<1, 128, 16384>>>(v.idesc, v.lbo, v.sbo, v.sw, d);
