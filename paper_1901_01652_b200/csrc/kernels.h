@@ -88,9 +88,9 @@ int stream_sketch_f32_grid(int64_t dim, int K, int64_t ncols, int num_sms, int* 
 int launch_stream_sketch_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
                              cudaStream_t s);
 bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols);
-// writes P^(1) in fp64 (the fp32 input's later modes then run the fp64 kernels)
-void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
-                           cudaStream_t s);
+// writes P^(1) in fp32 (or fp64 with f64_out)
+void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, bool f64_out, const double* q, int64_t ldq,
+                           int num_sms, cudaStream_t s);
 
 // ---- fp32 mode-0 sketch / shrink on tcgen05 (kind::tf32, 3xTF32, TMEM accumulators), tc_f32.cu
 bool tc_sketch_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
@@ -102,6 +102,14 @@ size_t tc_ttm_f32_scratch(int64_t dim, int64_t K);  // bytes of the split Q oper
 // out: P^(1) in fp64 (f64_out) or fp32; q: Q (ldq x K column-major fp64)
 void launch_tc_ttm_f32(const TTMPlan& p, const void* in, void* out, bool f64_out, const double* q, int64_t ldq,
                        float* scratch, int num_sms, cudaStream_t s);
+
+// ---- fp32 register-tiled FFMA kernels for modes with left > 1 (slab_f32.cu); fp32 in and out
+bool slab_f32_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right);
+void launch_slab_f32_ttm(const TTMPlan& p, const void* in, void* out, const double* m, int num_sms, cudaStream_t s);
+bool slab_f32_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t right);
+int slab_f32_sketch_grid(int64_t left, int64_t dim, int K, int64_t right, int num_sms);  // = partial count
+int launch_slab_f32_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                           cudaStream_t s);
 
 // ---- cp.async-gathered fp64 tensor-core kernels for modes with left > 1 (slab_f64.cu)
 bool slab_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);

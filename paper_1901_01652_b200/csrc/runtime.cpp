@@ -495,6 +495,13 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
             gc = trg::launch_stream_sketch_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
         }, yout ? 2 : 1);
         if (defer) *yp = YParts{partial, gc};
+    } else if (trg::slab_f32_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
+        const int gc = trg::slab_f32_sketch_grid(p.left, p.dim, (int)Kn, p.right, ctx->num_sms);
+        partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_slab_f32_sketch(p, cur, partial, yout, ctx->num_sms, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, gc};
     } else if (slab2) {
         const int NT = Kn <= 8 ? 1 : 2;
         double* om = nullptr;
@@ -537,9 +544,11 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
     ctx->allreduce(dYfull, (size_t)(x->dims[n] * Kn), F64);
 }
 
-// fp32 mode-0 shrinks write P^(1) in fp64 (the later modes then run the fp64 kernels)
+// fp32 inputs keep fp32 intermediates (the later modes run the fp32 slab kernels, slab_f32.cu);
+// TRG_PROMOTE_F64=1 restores the former fp64 P^(1) (development comparison)
 bool mode0_promotes(int dt, int64_t left, int64_t dim, int64_t K, int64_t right) {
-    return trg::tc_ttm_f32_ok(dt, left, dim, K, right) || trg::stream_ttm_f32_ok(dt, left, dim, K, right);
+    static const bool promote = getenv("TRG_PROMOTE_F64") != nullptr;
+    return promote && (trg::tc_ttm_f32_ok(dt, left, dim, K, right) || trg::stream_ttm_f32_ok(dt, left, dim, K, right));
 }
 
 // out = cur x_n Q^T (local rows of Q for the sharded last mode), new buffer.
@@ -562,6 +571,7 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
     const double* m = dQ;
     if (n == N - 1) m += x->lo;  // local rows of Q_{N-1}
     const bool tc = trg::tc_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right);
+    const bool f32s = trg::stream_ttm_f32_ok(p.dtype, p.left, p.dim, Kn, p.right);
     const bool promote = mode0_promotes(p.dtype, p.left, p.dim, Kn, p.right);
     *odt = promote ? F64 : cdt;
     const size_t es = trg::dtype_size(*odt);
@@ -572,9 +582,13 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
             trg::launch_tc_ttm_f32(p, cur, out, *odt == F64, m, x->dims[n], scratch, ctx->num_sms, ctx->stream);
         }, 2);
         ctx->tmp_free(scratch);
-    } else if (promote) {
+    } else if (f32s) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
-            trg::launch_stream_ttm_f32(p, cur, out, m, x->dims[n], ctx->num_sms, ctx->stream);
+            trg::launch_stream_ttm_f32(p, cur, out, promote, m, x->dims[n], ctx->num_sms, ctx->stream);
+        });
+    } else if (trg::slab_f32_ttm_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_slab_f32_ttm(p, cur, out, m, ctx->num_sms, ctx->stream);
         });
     } else if (trg::stream_ttm_ok(p.dtype, p.left, p.dim, Kn)) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {

@@ -294,7 +294,8 @@ struct F32TtArgs {
     int64_t I0, L;  // X_(0) is I0 x L (fibres of I0)
     int DC, NCH, K, Kp;  // K outputs in all (row stride of out); CTA row blockIdx.y owns KP of them
     int64_t nunits;  // ceil(L / 64)
-    double* out;     // P^(1) promoted to fp64: row m, K outputs (o fastest); later modes run fp64
+    void* out;       // P^(1): row m, K outputs (o fastest), fp32 (f64out = 0) or fp64
+    int f64out;
 };
 
 template <int KP>
@@ -393,10 +394,17 @@ __global__ void __launch_bounds__((kTtCons + 1) * 32, 1)
         for (int f = 0; f < 2; ++f) {
             const int64_t m = u * 64 + lane + 32 * f;
             if (m >= a.L) continue;
-            double* dst = a.out + m * a.K + ko;
+            if (a.f64out) {
+                double* dst = reinterpret_cast<double*>(a.out) + m * a.K + ko;
 #pragma unroll
-            for (int o = 0; o < KP; ++o)
-                if (ko + o < a.K) dst[o] = (double)acc[f][o];
+                for (int o = 0; o < KP; ++o)
+                    if (ko + o < a.K) dst[o] = (double)acc[f][o];
+            } else {
+                float* dst = reinterpret_cast<float*>(a.out) + m * a.K + ko;
+#pragma unroll
+                for (int o = 0; o < KP; ++o)
+                    if (ko + o < a.K) dst[o] = acc[f][o];
+            }
         }
     }
 }
@@ -547,8 +555,8 @@ bool stream_ttm_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t 
     return smem <= 220 * 1024;
 }
 
-void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, int num_sms,
-                           cudaStream_t s) {
+void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, bool f64_out, const double* q, int64_t ldq,
+                           int num_sms, cudaStream_t s) {
     F32TtArgs a{};
     a.I0 = p.dim;
     a.L = p.right;
@@ -557,7 +565,8 @@ void launch_stream_ttm_f32(const TTMPlan& p, const void* in, void* out, const do
     a.K = (int)p.odim;
     a.Kp = ttm_f32_kp(p.odim);
     a.nunits = (p.right + 63) / 64;
-    a.out = reinterpret_cast<double*>(out);
+    a.out = out;
+    a.f64out = f64_out ? 1 : 0;
     CUtensorMap map;
     const cuuint64_t gdim[2] = {(cuuint64_t)p.dim, (cuuint64_t)p.right};
     const cuuint64_t gstride[1] = {(cuuint64_t)p.dim * 4};
