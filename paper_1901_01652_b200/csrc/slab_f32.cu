@@ -168,17 +168,26 @@ struct SknArgs {
     int64_t rows_glob, col_off;
 };
 
-template <int KG>
+// 4-byte global -> shared copy (LDGSTS): the transposed slab lands without register staging
+__device__ __forceinline__ void cp4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+
+template <int KG, bool ASYNC>
 __global__ void __launch_bounds__(kThreads) k_sketch_n_f32(SknArgs a) {
     extern __shared__ __align__(16) float sm[];
-    // per group: P item [LC][pitch] (d fastest, odd pitch) and Omega [LC][KG] (16-byte aligned)
+    // per group: two P item buffers [LC][pitch] (d fastest, odd pitch: the transposed stores and
+    // the d reads are conflict-free) and Omega [LC][KG]; round j + 1's slab lands (cp.async)
+    // while round j is multiplied
     const int pfl = (a.LC * a.pitch + 3) & ~3;
-    const int item_floats = pfl + a.LC * KG;
+    constexpr int nbuf = ASYNC ? 2 : 1;
+    const int item_floats = nbuf * pfl + a.LC * KG;
     const int tid = threadIdx.x;
     const int g = tid / a.DQ, dq = tid - g * a.DQ;
     const bool active = g < a.G;
     float* Pg = sm + (size_t)(active ? g : 0) * item_floats;
-    float* Og = Pg + pfl;
+    float* Og = Pg + nbuf * pfl;
     const int k0 = blockIdx.y * KG;
     float acc[4][KG];
 #pragma unroll
@@ -187,15 +196,35 @@ __global__ void __launch_bounds__(kThreads) k_sketch_n_f32(SknArgs a) {
         for (int j = 0; j < KG; ++j) acc[i][j] = 0.f;
     // items (r, l-chunk) of this CTA: [it0, it1), taken G at a time (group g takes it + g)
     const int64_t it0 = a.nitems * blockIdx.x / gridDim.x, it1 = a.nitems * (blockIdx.x + 1) / gridDim.x;
-    for (int64_t base = it0; base < it1; base += a.G) {
-        __syncthreads();
+    auto issue = [&](int64_t base, int buf) {
         if (active && base + g < it1) {
             const int64_t item = base + g;
             const int64_t r = item / a.nlc;
             const int l0 = (int)(item - r * a.nlc) * a.LC;
             const int lc = min(a.LC, a.left - l0);
-            // P(l0 .. l0 + lc, :, r) -> Pg[l][d]: 16-byte reads along l (lc % 4 == 0), four in
-            // flight per thread, scattered into the transposed rows
+            const float* src = a.in + l0 + (int64_t)a.left * a.dim * r;
+            float* P = Pg + buf * pfl;
+            // (d, l) walked l fastest: coalesced reads, stores down the transposed rows
+            const int dstep = a.DQ / lc, lstep = a.DQ - dstep * lc;
+            for (int d = dq / lc, l = dq - (dq / lc) * lc; d < a.dim;) {
+                cp4(P + l * a.pitch + d, src + l + (int64_t)a.left * d);
+                d += dstep;
+                l += lstep;
+                if (l >= lc) {
+                    l -= lc;
+                    ++d;
+                }
+            }
+        }
+        cp_commit();
+    };
+    // register-staged variant: 16-byte reads along l, four in flight, scattered into the rows
+    auto load_now = [&](int64_t base) {
+        if (active && base + g < it1) {
+            const int64_t item = base + g;
+            const int64_t r = item / a.nlc;
+            const int l0 = (int)(item - r * a.nlc) * a.LC;
+            const int lc = min(a.LC, a.left - l0);
             const float* src = a.in + l0 + (int64_t)a.left * a.dim * r;
             const int q4 = lc >> 2, nq = q4 * a.dim;
             for (int q = dq; q < nq; q += 4 * a.DQ) {
@@ -218,6 +247,22 @@ __global__ void __launch_bounds__(kThreads) k_sketch_n_f32(SknArgs a) {
                         o[3 * a.pitch] = v[u].w;
                     }
             }
+        }
+    };
+    if (ASYNC) issue(it0, 0);
+    int rnd = 0;
+    for (int64_t base = it0; base < it1; base += a.G, ++rnd) {
+        const bool more = base + a.G < it1;
+        if (ASYNC) {
+            if (more) issue(base + a.G, (rnd + 1) & 1);
+        } else {
+            load_now(base);
+        }
+        if (active && base + g < it1) {
+            const int64_t item = base + g;
+            const int64_t r = item / a.nlc;
+            const int l0 = (int)(item - r * a.nlc) * a.LC;
+            const int lc = min(a.LC, a.left - l0);
             // Omega(col_off + l0 + l + left r, k0 + k) for l < lc, k < KG (zero outside K)
             const int npair = lc / 2 + 1;
             for (int e = dq; e < KG * npair; e += a.DQ) {
@@ -239,14 +284,21 @@ __global__ void __launch_bounds__(kThreads) k_sketch_n_f32(SknArgs a) {
                 }
             }
         }
+        if (ASYNC) {
+            if (more)
+                cp_wait<1>();
+            else
+                cp_wait<0>();
+        }
         __syncthreads();
         if (active && base + g < it1) {
             const int64_t item = base + g;
             const int l0 = (int)(item - (item / a.nlc) * a.nlc) * a.LC;
             const int lc = min(a.LC, a.left - l0);
+            const float* P = Pg + (ASYNC ? (rnd & 1) * pfl : 0);
             for (int l = 0; l < lc; ++l) {
                 // this thread's d = dq + i DQ: consecutive lanes, consecutive words (conflict-free)
-                const float* pr = Pg + l * a.pitch + dq;
+                const float* pr = P + l * a.pitch + dq;
                 const float pv[4] = {pr[0], pr[a.DQ], pr[2 * a.DQ], pr[3 * a.DQ]};
                 const float* orow = Og + l * KG;
 #pragma unroll
@@ -260,6 +312,7 @@ __global__ void __launch_bounds__(kThreads) k_sketch_n_f32(SknArgs a) {
                 }
             }
         }
+        __syncthreads();  // Og and this round's buffer are rewritten next
     }
     // groups -> one sum (fixed order), then this CTA's fp64 partial columns [k0, k0 + KG)
     __syncthreads();
@@ -311,6 +364,7 @@ bool plan_ttn(int64_t left, int64_t dim, int64_t K, int64_t right, TtnPlan& p) {
 
 struct SknPlan {
     int KG, ky, LC, G, DQ, pitch;
+    bool async;  // cp.async double buffering (one group, one k-group: C3) or register-staged loads
     int64_t nlc, nitems;
     size_t smem;
 };
@@ -324,14 +378,16 @@ bool plan_skn(int64_t left, int64_t dim, int K, int64_t right, SknPlan& p) {
     p.pitch = (int)(4 * p.DQ) | 1;  // odd: transposed stores and d reads conflict-free
     // l-chunk: the G items fit ~96 KB, and small when few (r, l) items would leave SMs idle
     // (C3 / C4 mode 2: left 400 / 4096 with right = 1)
-    const int64_t per_l = (int64_t)p.pitch + p.KG + 4;
+    p.async = p.G == 1 && p.ky == 1;
+    const int nbuf = p.async ? 2 : 1;
+    const int64_t per_l = nbuf * (int64_t)p.pitch + p.KG + 8;
     const int64_t lc_mem = std::max<int64_t>(1, (96 * 1024 / 4) / (p.G * per_l));
     const int64_t lc_par = std::max<int64_t>(1, (left * right + 2 * 148 * p.G - 1) / (2 * 148 * p.G));
     p.LC = (int)std::min<int64_t>(left, std::min(lc_mem, std::max<int64_t>(4, lc_par))) & ~3;
     if (p.LC < 4) return false;
     p.nlc = (left + p.LC - 1) / p.LC;
     p.nitems = right * p.nlc;
-    const size_t items = (size_t)p.G * (((p.LC * p.pitch + 3) & ~3) + p.LC * p.KG) * 4;
+    const size_t items = (size_t)p.G * (nbuf * ((p.LC * p.pitch + 3) & ~3) + p.LC * p.KG) * 4;
     const size_t red = (size_t)p.G * p.DQ * 4 * p.KG * 4;
     p.smem = std::max(items, red);
     return p.smem <= 160 * 1024;
@@ -406,10 +462,18 @@ int launch_slab_f32_sketch(const SketchPlan& sp, const void* x, double* partial,
     a.col_off = sp.col_off;
     const int gx = slab_f32_sketch_grid(sp.left, sp.dim, sp.K, sp.right, num_sms);
     const dim3 grid(gx, p.ky);
-#define TRG_SKN(KGV)                                                       \
-    do {                                                                   \
-        allow_smem(k_sketch_n_f32<KGV>, p.smem);                           \
-        k_sketch_n_f32<KGV><<<grid, kThreads, p.smem, s>>>(a);             \
+    // cp.async double buffering pays where one group streams long slabs (C3: 136 -> 91 us);
+    // with several groups or k-groups the register-staged loads measure faster (C4, C5)
+    const bool async = p.async;
+#define TRG_SKN(KGV)                                                               \
+    do {                                                                           \
+        if (async) {                                                               \
+            allow_smem(k_sketch_n_f32<KGV, true>, p.smem);                         \
+            k_sketch_n_f32<KGV, true><<<grid, kThreads, p.smem, s>>>(a);           \
+        } else {                                                                   \
+            allow_smem(k_sketch_n_f32<KGV, false>, p.smem);                        \
+            k_sketch_n_f32<KGV, false><<<grid, kThreads, p.smem, s>>>(a);          \
+        }                                                                          \
     } while (0)
     switch (p.KG) {
         case 4: TRG_SKN(4); break;
