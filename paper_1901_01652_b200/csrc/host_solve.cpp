@@ -90,6 +90,7 @@ Mat matmul_tn(const Mat& A, const Mat& B) {
             const double* ai = A.col(i);
             const double* bj = B.col(j);
             double s = 0.0;
+#pragma omp simd reduction(+ : s)
             for (idx k = 0; k < A.r; ++k) s += ai[k] * bj[k];
             C(i, j) = s;
         }
@@ -123,12 +124,56 @@ Tensor subchain(const Cores& f, idx mode) {
 }
 
 // ---------------------------------------------------------------- QR / LS
+// Blocked Householder kernels (compact WY): a panel of nb reflectors H_j = I - tau_j v_j v_j^T
+// (v_j(j) = 1, Eigen's makeHouseholder convention as in HQR below) is applied as
+// I - V T V^T with T upper triangular, so the trailing update is two GEMM-shaped passes over the
+// columns (W = V^T A, A -= V (T^T W)) instead of nb rank-1 passes: the same reflectors, so the
+// same R and Q^T b up to rounding (C4's 2048-4096 x 400 ALS least squares, solvers.hpp:195-205).
+#if defined(__GNUC__) && !defined(__clang__) && defined(__x86_64__)
+#define TRG_HOT __attribute__((target_clones("avx512f", "avx2", "default")))
+#else
+#define TRG_HOT
+#endif
+
+// W(0:nb, c) = V^T A(:, c) for rows [j0, m): V = panel columns j0 .. j0 + nb (unit diagonal,
+// zeros above), then A(:, c) -= V (T^T W(:, c))
+TRG_HOT void apply_block_col(const double* qr, idx ld, idx m, idx j0, idx nb, const double* T, double* a) {
+    double w[64];
+    for (idx p = 0; p < nb; ++p) {
+        const double* v = qr + ld * (j0 + p);
+        double s = a[j0 + p];  // unit diagonal
+#pragma omp simd reduction(+ : s)
+        for (idx i = j0 + p + 1; i < m; ++i) s += v[i] * a[i];
+        w[p] = s;
+    }
+    double y[64];  // y = T^T w
+    for (idx p = 0; p < nb; ++p) {
+        double s = 0.0;
+        for (idx q = 0; q <= p; ++q) s += T[q + nb * p] * w[q];
+        y[p] = s;
+    }
+    for (idx p = 0; p < nb; ++p) {
+        const double* v = qr + ld * (j0 + p);
+        const double yp = y[p];
+        a[j0 + p] -= yp;
+        for (idx i = j0 + p + 1; i < m; ++i) a[i] -= yp * v[i];
+    }
+}
+
 struct HQR {
     Mat qr;
     std::vector<double> tau;
+    static constexpr idx kNb = 32;
+    bool blocked = false;
+    std::vector<std::vector<double>> Ts;  // per panel T (nb x nb, column-major)
     explicit HQR(const Mat& a) : qr(a) {
         const idx m = qr.r, n = qr.c, k = std::min(m, n);
         tau.assign(static_cast<size_t>(k), 0.0);
+        blocked = n >= 2 * kNb && m * n >= (1 << 16);
+        if (blocked) {
+            factor_blocked();
+            return;
+        }
         for (idx j = 0; j < k; ++j) {
             double* cj = qr.col(j);
             const double c0 = cj[j];
@@ -160,9 +205,82 @@ struct HQR {
             }
         }
     }
+    // one Householder step at column j, updating only columns (j, cend)
+    void reflect(idx j, idx cend) {
+        const idx m = qr.r;
+        double* cj = qr.col(j);
+        const double c0 = cj[j];
+        double tail = 0.0;
+#pragma omp simd reduction(+ : tail)
+        for (idx i = j + 1; i < m; ++i) tail += cj[i] * cj[i];
+        double beta, t;
+        if (tail <= std::numeric_limits<double>::min()) {  // Eigen makeHouseholder
+            t = 0.0;
+            beta = c0;
+            for (idx i = j + 1; i < m; ++i) cj[i] = 0.0;
+        } else {
+            beta = std::sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0) beta = -beta;
+            const double inv = 1.0 / (c0 - beta);
+            for (idx i = j + 1; i < m; ++i) cj[i] *= inv;
+            t = (beta - c0) / beta;
+        }
+        cj[j] = beta;
+        tau[static_cast<size_t>(j)] = t;
+        if (t == 0.0) return;
+        for (idx c = j + 1; c < cend; ++c) {
+            double* cc = qr.col(c);
+            double w = cc[j];
+#pragma omp simd reduction(+ : w)
+            for (idx i = j + 1; i < m; ++i) w += cj[i] * cc[i];
+            w *= t;
+            cc[j] -= w;
+            for (idx i = j + 1; i < m; ++i) cc[i] -= w * cj[i];
+        }
+    }
+    void factor_blocked() {
+        const idx m = qr.r, n = qr.c, k = std::min(m, n);
+        for (idx j0 = 0; j0 < k; j0 += kNb) {
+            const idx nb = std::min(kNb, k - j0);
+            for (idx j = j0; j < j0 + nb; ++j) reflect(j, j0 + nb);  // the panel
+            // T: T(0:p, p) = -tau_p T(0:p, 0:p) V(:, 0:p)^T v_p, T(p, p) = tau_p
+            std::vector<double> T(static_cast<size_t>(nb * nb), 0.0);
+            for (idx p = 0; p < nb; ++p) {
+                const double tp = tau[static_cast<size_t>(j0 + p)];
+                const double* vp = qr.col(j0 + p);
+                std::vector<double> z(static_cast<size_t>(p), 0.0);
+                for (idx q = 0; q < p; ++q) {  // (V_q)^T v_p over rows >= j0 + p (v_p is zero above, 1 at j0 + p)
+                    const double* vq = qr.col(j0 + q);
+                    double s2 = vq[j0 + p];
+#pragma omp simd reduction(+ : s2)
+                    for (idx i = j0 + p + 1; i < m; ++i) s2 += vq[i] * vp[i];
+                    z[static_cast<size_t>(q)] = s2;
+                }
+                for (idx q = 0; q < p; ++q) {
+                    double s2 = 0.0;
+                    for (idx r = q; r < p; ++r) s2 += T[static_cast<size_t>(q + nb * r)] * z[static_cast<size_t>(r)];
+                    T[static_cast<size_t>(q + nb * p)] = -tp * s2;
+                }
+                T[static_cast<size_t>(p + nb * p)] = tp;
+            }
+            const double* Tp = T.data();
+#pragma omp parallel for schedule(static)
+            for (idx c = j0 + nb; c < n; ++c) apply_block_col(qr.a.data(), m, m, j0, nb, Tp, qr.col(c));
+            Ts.push_back(std::move(T));
+        }
+    }
     Mat solve(const Mat& b) const {
         const idx m = qr.r, n = qr.c, k = static_cast<idx>(tau.size());
         Mat y = b;
+        if (blocked) {
+            for (idx j0 = 0, p = 0; j0 < k; j0 += kNb, ++p) {
+                const idx nb = std::min(kNb, k - j0);
+                const double* Tp = Ts[static_cast<size_t>(p)].data();
+#pragma omp parallel for schedule(static) if (y.c * (m - j0) > (1 << 15))
+                for (idx c = 0; c < y.c; ++c) apply_block_col(qr.a.data(), m, m, j0, nb, Tp, y.col(c));
+            }
+            return back_substitute(y, b.c);
+        }
         for (idx j = 0; j < k; ++j) {
             const double t = tau[static_cast<size_t>(j)];
             if (t == 0.0) continue;
@@ -177,9 +295,13 @@ struct HQR {
                 for (idx i = j + 1; i < m; ++i) bc[i] -= w * v[i];
             }
         }
-        Mat x(n, b.c);
-#pragma omp parallel for schedule(static) if (b.c * n * n > (1 << 16))
-        for (idx c = 0; c < b.c; ++c)
+        return back_substitute(y, b.c);
+    }
+    Mat back_substitute(const Mat& y, idx nc) const {
+        const idx n = qr.c;
+        Mat x(n, nc);
+#pragma omp parallel for schedule(static) if (nc * n * n > (1 << 16))
+        for (idx c = 0; c < nc; ++c)
             for (idx i = n - 1; i >= 0; --i) {
                 double s = y(i, c);
                 for (idx j = i + 1; j < n; ++j) s -= qr(i, j) * x(j, c);
