@@ -7,6 +7,7 @@ Each CUDA / C++ source is compiled by nvcc with
 paper_1901_01652_b200/libtrg.so (git-ignored, travels to the GPU box with
 gpurun). Objects are rebuilt only when a source or header is newer.
 """
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -17,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtrg.so")
 
-SOURCES = ["sketch.cu", "stream_f64.cu", "slab_f64.cu", "slab_tma.cu", "stream_f32.cu", "tc_f32.cu", "slab_f32.cu", "ttm.cu", "qr.cu", "tr.cu", "runtime.cpp", "host_solve.cpp"]
+SOURCES = ["sketch.cu", "stream_f64.cu", "slab_f64.cu", "slab_tma.cu", "stream_f32.cu", "tc_f32.cu", "slab_f32.cu", "slab_st.cu", "ttm.cu", "qr.cu", "tr.cu", "runtime.cpp", "host_solve.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -47,16 +48,20 @@ def _newer(src, dst, deps):
 def build(verbose=False):
     os.makedirs(BUILD, exist_ok=True)
     deps = _headers()
-    objs = []
+    objs, cmds = [], []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
         objs.append(obj)
         if _newer(src, obj, deps):
-            cmd = [NVCC] + _flags() + ["-c", src, "-o", obj]
-            if verbose:
-                print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append([NVCC] + _flags() + ["-c", src, "-o", obj])
+    # one nvcc per translation unit, in parallel (each is single-threaded)
+    jobs = max(1, min(len(cmds), os.cpu_count() or 1))
+    with concurrent.futures.ThreadPoolExecutor(jobs) as ex:
+        for cmd, rc in zip(cmds, ex.map(lambda c: (print(" ".join(c), flush=True) if verbose else None,
+                                                   subprocess.run(c).returncode)[1], cmds)):
+            if rc != 0:
+                raise subprocess.CalledProcessError(rc, cmd)
     if any(_newer(o, LIB, []) for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-Xcompiler", "-fopenmp", "-ldl", "-lgomp"]
         if verbose:

@@ -61,3 +61,35 @@ def test_qr_wide_k_uses_householder_kernel(trg):
 def test_qr_errors(trg):
     with pytest.raises(ValueError):
         trg.economy_q(np.zeros((3, 5)))
+
+
+@pytest.mark.parametrize("m,k", [(1000, 20), (1024, 64), (200, 32)])
+def test_qr_cluster_ill_conditioned_falls_back(trg, m, k):
+    """K_n > 16 runs the cluster CholQR2; cond 1e9 must reach the Householder fallback (rank 0)."""
+    rng = np.random.default_rng(m + k)
+    u, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    v, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    y = u @ np.diag(np.logspace(0, -9, k)) @ v.T
+    q, path = trg.economy_q(y, return_path=True)
+    assert path == 1
+    assert np.abs(q - orc.economy_q(y)).max() < 1e-6
+
+
+def test_qr_cluster_rank_deficient(trg):
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((300, 5)) @ rng.standard_normal((5, 24))  # rank 5 < 24
+    q, path = trg.economy_q(y, return_path=True)
+    assert path == 1
+    assert np.abs(q[:, :5] - orc.economy_q(y)[:, :5]).max() < 1e-10
+
+
+def test_qr_cluster_moderate_condition_two_passes(trg):
+    """cond 1e4: CholQR's first pass is not orthonormal to 1e-13, the second pass must run."""
+    rng = np.random.default_rng(6)
+    u, _ = np.linalg.qr(rng.standard_normal((1024, 64)))
+    v, _ = np.linalg.qr(rng.standard_normal((64, 64)))
+    y = u @ np.diag(np.logspace(0, -4, 64)) @ v.T
+    q, path = trg.economy_q(y, return_path=True)
+    assert path == 0
+    assert np.abs(q.T @ q - np.eye(64)).max() < 1e-13
+    assert np.abs(q - orc.economy_q(y)).max() < 1e-10

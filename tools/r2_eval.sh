@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round-2 evaluation pass on the GPU box: GPU tests (with per-config parity records), the
+# default bench line, one bench line per config, a launch list and a full capture of C2.
+cd $GRAFT_REPO_ROOT
+tag=${1:-r2a}
+nvidia-smi > gpurun_out/${tag}_smi.txt 2>&1
+rm -f gpurun_out/${tag}_parity.jsonl
+TRG_PARITY_OUT=gpurun_out/${tag}_parity.jsonl timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/${tag}_gputest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/${tag}_gputest.log
+timeout 600 python bench.py > gpurun_out/${tag}_bench_c2.log 2>&1
+for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 20 --warmup 3 --e2e-steps 2 --no-cpu-baseline > gpurun_out/${tag}_cfg_$c.log 2>&1; done
+for c in c2 c3 c4 c5; do
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches_$c.csv \
+    python bench.py --config $c --steps 2 --warmup 3 --e2e-steps 0 --decompose 0 --no-cpu-baseline > gpurun_out/${tag}_ncu_l_$c.log 2>&1
+done
+echo done
