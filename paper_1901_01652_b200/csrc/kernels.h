@@ -111,6 +111,18 @@ int slab_f32_sketch_grid(int64_t left, int64_t dim, int K, int64_t right, int nu
 int launch_slab_f32_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
                            cudaStream_t s);
 
+// ---- fp32 TMA-streamed FFMA kernels for modes with left > 1 (slab_st.cu): producer warp + mbarrier
+// ring of 3-D boxes, generator warps for the sketch's test-matrix blocks
+bool st_shrink_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right);
+void launch_st_shrink(const TTMPlan& p, const void* in, void* out, const double* m, int num_sms, cudaStream_t s);
+bool st_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t right);
+int st_sketch_grid(int64_t left, int64_t dim, int K, int64_t right, int num_sms);  // = partial count
+int launch_st_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms, cudaStream_t s);
+
+// mode-0 shrink of a short-fibre fp32 tensor (left == 1, dim <= 128, dim % 4 == 0; C5): bulk-copied fibres
+bool st0_shrink_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t ncols);
+void launch_st0_shrink(const TTMPlan& p, const void* in, void* out, const double* m, int num_sms, cudaStream_t s);
+
 // ---- cp.async-gathered fp64 tensor-core kernels for modes with left > 1 (slab_f64.cu)
 bool slab_sketch_ok(int dtype, int64_t left, int64_t dim, int K, int64_t ncols);
 void launch_slab_sketch(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,

@@ -495,6 +495,13 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
             gc = trg::launch_stream_sketch_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
         }, yout ? 2 : 1);
         if (defer) *yp = YParts{partial, gc};
+    } else if (trg::st_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
+        const int gc = trg::st_sketch_grid(p.left, p.dim, (int)Kn, p.right, ctx->num_sms);
+        partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_st_sketch(p, cur, partial, yout, ctx->num_sms, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, gc};
     } else if (trg::slab_f32_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
         const int gc = trg::slab_f32_sketch_grid(p.left, p.dim, (int)Kn, p.right, ctx->num_sms);
         partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
@@ -582,10 +589,18 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
             trg::launch_tc_ttm_f32(p, cur, out, *odt == F64, m, x->dims[n], scratch, ctx->num_sms, ctx->stream);
         }, 2);
         ctx->tmp_free(scratch);
+    } else if (!promote && trg::st0_shrink_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_st0_shrink(p, cur, out, m, ctx->num_sms, ctx->stream);
+        }, 2);
     } else if (f32s) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_stream_ttm_f32(p, cur, out, promote, m, x->dims[n], ctx->num_sms, ctx->stream);
         });
+    } else if (trg::st_shrink_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_st_shrink(p, cur, out, m, ctx->num_sms, ctx->stream);
+        }, 2);
     } else if (trg::slab_f32_ttm_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_slab_f32_ttm(p, cur, out, m, ctx->num_sms, ctx->stream);

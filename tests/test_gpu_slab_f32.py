@@ -30,6 +30,13 @@ CASES = [
     ((16, 37, 23), (16, 5, 3)),         # odd dim, K
     ((8, 100, 11), (8, 33, 4)),         # K = 33 -> two k-groups
     ((4, 7, 300), (4, 1, 3)),           # K = 1 (and mode 2 with K <= rank 4 of its unfolding)
+    ((12, 12, 60, 30), (12, 12, 12, 7)),  # left 144 in l-blocks, partial slab blocks (slab_st.cu)
+    ((20, 400, 33), (20, 20, 9)),       # d-chunks over several CTA groups, ragged right
+    ((6, 50, 40), (6, 10, 5)),          # left 6: not a multiple of 4 (the slab_f32.cu kernels)
+    ((1728, 60), (1728, 12)),           # left 1728, right 1 (C5's mode-4 shape class)
+    ((60, 60, 30), (12, 60, 30)),       # mode 0 only, short fibres (slab_st.cu k_st0_*: C5's mode 0)
+    ((400, 50, 21), (20, 50, 21)),      # mode-0 sketch with long fibres, K 20 (C3's mode-0 class)
+    ((1000, 7, 9), (20, 7, 9)),         # C3's I_0 = 1000 with few columns (partial fibre stages)
 ]
 
 

@@ -1,0 +1,15 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+tag=${1:-r2f}
+timeout 300 python tools/qr_probe_c4.py c4 > gpurun_out/${tag}_qrprobe.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:qr --csv --log-file gpurun_out/${tag}_qrprobe.csv python tools/qr_probe_c4.py c4 > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_gpu_qr.py tests/test_gpu_slab_f32.py -q -x > gpurun_out/${tag}_test.log 2>&1
+echo "rc=$?" >> gpurun_out/${tag}_test.log
+timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_loopback.py tests/test_gpu_parity.py -q -x > gpurun_out/${tag}_cfgtest.log 2>&1
+echo "rc=$?" >> gpurun_out/${tag}_cfgtest.log
+for c in c3 c4 c5; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --e2e-steps 0 --decompose 0 --no-cpu-baseline > gpurun_out/${tag}_cfg_$c.log 2>&1; done
+for c in c3 c4 c5; do
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches_$c.csv \
+    python bench.py --config $c --steps 2 --warmup 3 --e2e-steps 0 --decompose 0 --no-cpu-baseline > /dev/null 2>&1
+done
+echo done
