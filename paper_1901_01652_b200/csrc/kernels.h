@@ -197,6 +197,7 @@ void launch_chain(const double* a, int64_t ra, int64_t p, int64_t rb, const doub
 // mode 0 writes X (dtype) ; mode 1 accumulates per-block (sum (x - xhat)^2, sum x^2).
 struct ReconPlan {
     int dtype;
+    int write_mode;  // 1: synthesis (X := Xhat), 0: RSE sums (fp32 tensors: the FFMA GEMM k_rse_f32), 2: RSE in fp64
     int64_t I0, P, R0, R1;
     int grid_x, grid_y, threads;
     size_t smem;

@@ -91,58 +91,53 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 
 // Gaussians of `nruns` runs of `len` consecutive test-matrix columns: column c of run q is reference
-// draw g0(q) + c (sketch.hpp:32-38). Work unit = (run, chunk of ppt Box-Muller pairs); along a
-// chunk the SplitMix64 state advances by 2 gamma per pair (random.hpp:19), so a pair costs the
-// two output mixes and the fp32 Box-Muller only; four pairs are in flight per thread.
-// info(q) -> {g0, live (else zeros), base}; put(base, c, z) stores column c of the run.
+// draw g0(q) + c (sketch.hpp:32-38). A unit is one Box-Muller pair (draws 2p, 2p + 1; random.hpp:50-62)
+// of a run, the units are dealt round-robin over all nthreads threads (every warp gets its share:
+// the consumer warps generate between their multiplications) and each thread keeps two pairs in
+// flight. info(q) -> {g0, live (else zeros), base}; put(base, c, z) stores column c of the run.
 struct RunInfo {
     uint64_t g0;
     bool live;
     int base;
 };
 template <class Info, class Put>
-__device__ __forceinline__ void gen_runs(int g, int nthreads, int nruns, int len, int nch, int ppt, const FastDiv& div_nch,
-                                         uint64_t seed, Info info, Put put) {
+__device__ __forceinline__ void gen_runs(int g, int nthreads, int nruns, int len, const FastDiv& div_npr, uint64_t seed,
+                                         Info info, Put put) {
     constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
-    const int units = nruns * nch;
-    for (int u = g; u < units; u += nthreads) {
-        const int q = (int)div_nch.div((uint32_t)u);
-        const int ch = u - q * nch;
-        const RunInfo ri = info(q);
-        const uint64_t pbeg = (ri.g0 >> 1) + (uint64_t)ch * ppt;
-        const uint64_t plast = (ri.g0 + (uint64_t)len - 1) >> 1;
-        if (pbeg > plast) continue;
-        const int cnt = (int)((plast - pbeg + 1) < (uint64_t)ppt ? (plast - pbeg + 1) : (uint64_t)ppt);
-        uint64_t st = seed + (2ull * pbeg + 1ull) * kGamma;
-        int c = (int)(2 * pbeg - ri.g0);  // column of the first draw of pair pbeg (-1 when g0 is odd)
-        for (int i = 0; i < cnt; i += 4, st += 8ull * kGamma, c += 8) {
-            float z[4][2];
+    const int npr = len / 2 + 1;  // pairs touching a run of len columns
+    const int units = nruns * npr;
+    for (int u0 = g; u0 < units; u0 += 2 * nthreads) {
+        uint64_t st[2];
+        int cf[2], base[2];
+        bool on[2], live[2];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) gauss_pair_f32_fast(st + 2ull * j * kGamma, z[j][0], z[j][1]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    const int cc = c + 2 * j + v;
-                    if (i + j < cnt && cc >= 0 && cc < len) put(ri.base, cc, ri.live ? z[j][v] : 0.f);
-                }
+        for (int j = 0; j < 2; ++j) {
+            const int u = min(u0 + j * nthreads, units - 1);
+            const int q = (int)div_npr.div((uint32_t)u);
+            const int pi = u - q * npr;
+            const RunInfo ri = info(q);
+            const uint64_t p = (ri.g0 >> 1) + (uint64_t)pi;
+            cf[j] = (int)(2 * p - ri.g0);  // column of draw 2p (-1 when g0 is odd)
+            st[j] = seed + (2ull * p + 1ull) * kGamma;
+            on[j] = u0 + j * nthreads < units && cf[j] < len;
+            live[j] = ri.live;
+            base[j] = ri.base;
         }
+        float z[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) gauss_pair_f32_fast(st[j], z[j][0], z[j][1]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int cc = cf[j] + v;
+                if (on[j] && cc >= 0 && cc < len) put(base[j], cc, live[j] ? z[j][v] : 0.f);
+            }
     }
-}
-
-// chunking of nruns runs of len columns over nthreads generator threads
-__host__ inline void plan_gen(int nruns, int len, int nthreads, int* ppt, int* nch) {
-    const int npmax = len / 2 + 1;
-    const int64_t total = (int64_t)nruns * npmax;
-    int p = (int)std::max<int64_t>(4, (total + nthreads - 1) / nthreads);
-    p = (p + 3) & ~3;
-    *ppt = p;
-    *nch = (npmax + p - 1) / p;
 }
 
 constexpr int kStMaxStages = 8;
 constexpr int kStCons = 256;  // consumer threads (8 warps)
-constexpr int kStGen = 128;   // generator threads of the sketch (4 warps)
 
 // ================================================================== shrink
 struct StShArgs {
@@ -340,21 +335,20 @@ struct StSkArgs {
     uint32_t p_floats, stage_floats, om_floats;
     uint64_t seed, D;
     int64_t rows_glob, col_off;
-    FastDiv div_nch, div_rb;  // generator chunks per run; RB
-    int nch, ppt;
+    FastDiv div_npr, div_rb;  // Box-Muller pairs per column run; RB
 };
 
 template <int KG, int D>
-__global__ void __launch_bounds__(kStCons + kStGen + 32, 1) k_st_sketch(const __grid_constant__ CUtensorMap pmap,
-                                                                      StSkArgs a) {
+__global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_constant__ CUtensorMap pmap, StSkArgs a) {
     constexpr int KQ = KG / 4;
+    constexpr int kOR = 3;  // test-matrix ring: item n + 2 is generated while item n is multiplied
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + kStMaxStages;
     uint64_t* ofull = empty + kStMaxStages;
-    uint64_t* oempty = ofull + 2;
+    uint64_t* oempty = ofull + kOR;
     float* stg = reinterpret_cast<float*>(smem_raw + 256);
-    float* om = stg + (size_t)a.stages * a.stage_floats;  // 2 x om_floats
+    float* om = stg + (size_t)a.stages * a.stage_floats;  // kOR x om_floats
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t it0 = a.nitems * blockIdx.x / gridDim.x, it1 = a.nitems * (blockIdx.x + 1) / gridDim.x;
     const int k0 = blockIdx.y * KG, d0 = blockIdx.z * a.DC;
@@ -363,14 +357,14 @@ __global__ void __launch_bounds__(kStCons + kStGen + 32, 1) k_st_sketch(const __
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kStCons / 32);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&ofull[s], kStGen / 32);
+        for (int s = 0; s < kOR; ++s) {
+            mbar_init(&ofull[s], kStCons / 32);
             mbar_init(&oempty[s], kStCons / 32);
         }
         fence_mbar_init();
     }
     __syncthreads();
-    if (warp == (kStCons + kStGen) / 32) {  // producer
+    if (warp == kStCons / 32) {  // producer
         griddep_wait();
         if (lane == 0) {
             const uint64_t pol = policy_l2(0);
@@ -386,30 +380,27 @@ __global__ void __launch_bounds__(kStCons + kStGen + 32, 1) k_st_sketch(const __
         }
         return;
     }
-    if (tid >= kStCons) {  // generators: the item's Omega block [rl][l / 4][kq][l % 4][4] (rows padded)
-        const int g = tid - kStCons;
-        uint32_t n = 0;
-        for (int64_t it = it0; it < it1; ++it, ++n) {
-            const int64_t rbk = it / a.nlb;
-            const int lb = (int)(it - rbk * a.nlb);
-            const int s = (int)(n & 1);
-            if (n >= 2) mbar_wait_hint(&oempty[s], ((n >> 1) - 1) & 1);
-            float* O = om + (size_t)s * a.om_floats;
-            const int l0 = lb * a.LB;
-            gen_runs(g, kStGen, KG * a.RB, a.LB, a.nch, a.ppt, a.div_nch, a.seed,
-                     [&](int q) {
-                         const int k = (int)a.div_rb.div((uint32_t)q), rl = q - k * a.RB;
-                         const int64_t r = rbk * a.RB + rl;
-                         return RunInfo{a.D + (uint64_t)(a.col_off + l0 + (int64_t)a.left * r) +
-                                            (uint64_t)a.rows_glob * (uint64_t)(k0 + k),
-                                        k0 + k < a.K && r < a.right, rl * a.NLQ * a.ompitch + (k >> 2) * 16 + (k & 3)};
-                     },
-                     [&](int base, int c, float z) { O[base + (c >> 2) * a.ompitch + (c & 3) * 4] = z; });
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ofull[s]);
-        }
-        return;
-    }
+    // The consumer warps also generate the test-matrix blocks, two items ahead: the Box-Muller
+    // work (K / dim Gaussians per element, C5: 0.2) spreads over all of them instead of being the
+    // critical path of a few generator warps. Block layout [rl][l / 4][kq][l % 4][4] (rows padded).
+    auto generate = [&](int64_t it, uint32_t n) {
+        const int64_t rbk = it / a.nlb;
+        const int lb = (int)(it - rbk * a.nlb);
+        float* O = om + (size_t)(n % kOR) * a.om_floats;
+        const int l0 = lb * a.LB;
+        gen_runs(tid, kStCons, KG * a.RB, a.LB, a.div_npr, a.seed,
+                 [&](int q) {
+                     const int k = (int)a.div_rb.div((uint32_t)q), rl = q - k * a.RB;
+                     const int64_t r = rbk * a.RB + rl;
+                     return RunInfo{a.D + (uint64_t)(a.col_off + l0 + (int64_t)a.left * r) +
+                                        (uint64_t)a.rows_glob * (uint64_t)(k0 + k),
+                                    k0 + k < a.K && r < a.right, rl * a.NLQ * a.ompitch + (k >> 2) * 16 + (k & 3)};
+                 },
+                 [&](int base, int c, float z) { O[base + (c >> 2) * a.ompitch + (c & 3) * 4] = z; });
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofull[n % kOR]);
+    };
+    for (uint32_t j = 0; j < 2 && it0 + j < it1; ++j) generate(it0 + j, j);
     // consumers: thread = (rs, dl, lq), lq fastest: the P loads of a warp are consecutive 16-byte
     // chunks ([r][d][l] with d = dl + NDL i), the Omega loads broadcast over dl
     const int per = a.NLQ * a.NDL;
@@ -423,9 +414,9 @@ __global__ void __launch_bounds__(kStCons + kStGen + 32, 1) k_st_sketch(const __
         for (int j = 0; j < KG; ++j) acc[i][j] = 0.f;
     uint32_t n = 0;
     for (int64_t it = it0; it < it1; ++it, ++n) {
-        const int s = (int)(n % (uint32_t)a.stages), os = (int)(n & 1);
+        const int s = (int)(n % (uint32_t)a.stages), os = (int)(n % kOR);
         mbar_wait_hint(&full[s], (n / a.stages) & 1);
-        mbar_wait_hint(&ofull[os], (n >> 1) & 1);
+        mbar_wait_hint(&ofull[os], (n / kOR) & 1);
         if (active) {
             const float* P = stg + (size_t)s * a.stage_floats + 4 * lq;
             const float* O = om + (size_t)os * a.om_floats + (size_t)lq * a.ompitch;
@@ -469,6 +460,11 @@ __global__ void __launch_bounds__(kStCons + kStGen + 32, 1) k_st_sketch(const __
         if (lane == 0) {
             mbar_arrive(&empty[s]);
             mbar_arrive(&oempty[os]);
+        }
+        if (it + 2 < it1) {
+            // item n + 2 goes to the slot of item n - 1: every warp must be done with that one
+            if (n >= 1) mbar_wait_hint(&oempty[(n + 2) % kOR], ((n - 1) / kOR) & 1);
+            generate(it + 2, n + 2);
         }
     }
     // (rs, lq) partial sums -> this CTA's fp64 partial of (d-chunk, k-group), fixed order
@@ -537,7 +533,7 @@ bool plan_st_sketch(int64_t left, int64_t dim, int K, int64_t right, int num_sms
     p.npmax = p.LB / 2 + 1;
     if ((int64_t)p.KG * p.RB * p.npmax >= (int64_t(1) << 31)) return false;
     const size_t red = 4ull * (size_t)p.RS * p.NLQ * p.DC * p.KG;
-    const size_t stage_bytes = 4ull * p.stage_floats, om_bytes = 2ull * 4 * p.om_floats;
+    const size_t stage_bytes = 4ull * p.stage_floats, om_bytes = 3ull * 4 * p.om_floats;
     p.stages = (int)std::min<size_t>(kStMaxStages, (200 * 1024 - om_bytes) / stage_bytes);
     if (p.stages < 2) return false;
     p.stages = std::min(p.stages, 6);
@@ -556,8 +552,9 @@ bool plan_st_sketch(int64_t left, int64_t dim, int K, int64_t right, int num_sms
 // 1-D bulk copy. out(k, r) = sum_d X(d, r) Q(d, k); Q^T resident; thread = (k quad, four fibres
 // r + RB/4 i): per 4 d four 16-byte fibre loads, four broadcast 16-byte Q^T loads, 64 FFMA. Fibre
 // rows are 15 x 16 B apart for dim = 60: the 8 lanes of a load phase hit 8 different 16-byte bank
-// groups. (A matching mode-0 sketch with the same staging measured 1.8 ms against 1.1 ms for
-// stream_f32.cu's k_sketch_l1_f32 on C5 and is not kept.)
+// groups. (A mode-0 sketch with the same staging, its test matrix generated by dedicated warps or by
+// the consumer warps, measured 1.37-1.8 ms against 1.10 ms for stream_f32.cu's k_sketch_l1_f32 on
+// C5: K / I_0 = 0.2 Gaussians per element cost as much issue as the 12 FFMA, and it is not kept.)
 struct St0ShArgs {
     const float* x;
     float* out;
@@ -782,10 +779,9 @@ int launch_st_sketch(const SketchPlan& sp, const void* x, double* partial, doubl
     a.D = sp.D;
     a.rows_glob = sp.rows_glob;
     a.col_off = sp.col_off;
-    plan_gen(p.KG * p.RB, p.LB, kStGen, &a.ppt, &a.nch);
-    a.div_nch = FastDiv((uint32_t)a.nch);
+    a.div_npr = FastDiv((uint32_t)(p.LB / 2 + 1));
     a.div_rb = FastDiv((uint32_t)p.RB);
-    const dim3 grid(p.gx, p.ngroups, p.nz), block(kStCons + kStGen + 32);
+    const dim3 grid(p.gx, p.ngroups, p.nz), block(kStCons + 32);
 #define TRG_STSK(KGV, DV)                                               \
     do {                                                                \
         allow_smem(k_st_sketch<KGV, DV>, p.smem);                       \

@@ -11,6 +11,7 @@
 // G0(a, i0, b) S(b, p, a) with the (x - xhat)^2 and x^2 sums fused into its
 // epilogue, so Xhat is never written (RSE) — or is written as X (synthesis).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -131,6 +132,181 @@ __global__ void __launch_bounds__(256) k_recon(const double* __restrict__ g0, co
     }
 }
 
+
+// ---- K8 for fp32 tensors: Xhat(i0, p) = sum_{a,b} G0(a, i0, b) S(b, p, a) (tr_factors.hpp:123-137) as a
+// register-tiled FFMA GEMM on fp32 operands (the tensor is fp32; the RSE tolerance is 1e-4), with
+// sum (x - xhat)^2 and x^2 accumulated in fp64 in the epilogue (solvers.hpp:47-54). The operands
+// are first rounded and laid out K-major by two small passes: At[q][i0] and St[q][p] with
+// q = b + R1 a, so every tile row is contiguous and streams by 16-byte cp.async into a 3-stage ring.
+// M = I0 rows (tile MT = 128 or 64), N = the subchain's columns p (tile 128), K in chunks of 16.
+constexpr int kRkc = 16;
+constexpr int kRst = 3;
+
+__global__ void k_rse_prep_a(const double* __restrict__ g0, int64_t I0, int R0, int R1, int64_t ld,
+                             float* __restrict__ At) {
+    const int64_t n = (int64_t)R0 * R1 * ld;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = e / ld, i0 = e - q * ld;
+        const int a = (int)(q / R1), b = (int)(q - (int64_t)a * R1);
+        At[e] = i0 < I0 ? (float)g0[a + (int64_t)R0 * (i0 + I0 * b)] : 0.f;
+    }
+}
+
+// St[q][p] (row pitch ld >= P, zero padded) from S[b + R1 (p + P a)]: 32 x 32 tiles through shared memory
+__global__ void k_rse_prep_s(const double* __restrict__ S, int64_t P, int R0, int R1, int64_t ld, float* __restrict__ St) {
+    __shared__ float t[32][33];
+    const int K = R0 * R1;
+    const int64_t p0 = (int64_t)blockIdx.x * 32;
+    const int q0 = blockIdx.y * 32;
+    // read: q fastest within a (b contiguous in S)
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int64_t p = p0 + j;
+        const int q = q0 + threadIdx.x;
+        float v = 0.f;
+        if (q < K && p < P) {
+            const int a = q / R1, b = q - a * R1;
+            v = (float)S[b + (int64_t)R1 * (p + P * a)];
+        }
+        t[threadIdx.x][j] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int q = q0 + j;
+        const int64_t p = p0 + threadIdx.x;
+        if (q < K && p < ld) St[(int64_t)q * ld + p] = t[j][threadIdx.x];
+    }
+}
+
+__device__ __forceinline__ void cp16_rse(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+
+template <int MT>
+__global__ void __launch_bounds__(256, MT == 64 ? 2 : 1) k_rse_f32(const float* __restrict__ At, int64_t lda, const float* __restrict__ St,
+                                                 int64_t ldb, const float* __restrict__ x, int64_t I0, int64_t P, int K,
+                                                 double* __restrict__ block_sums) {
+    constexpr int TM = MT / 16;  // rows per thread
+    constexpr int NT = 128;
+    __shared__ __align__(16) float As[kRst][kRkc][MT];
+    __shared__ __align__(16) float Bs[kRst][kRkc][NT];
+    double* red = reinterpret_cast<double*>(&As[0][0][0]);  // [2][8], after the main loop
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;  // columns 8 tx.., rows TM ty..
+    const int64_t i_base = (int64_t)blockIdx.y * MT;
+    const int64_t p_base = (int64_t)blockIdx.x * NT;
+    const int nch = (K + kRkc - 1) / kRkc;  // At / St rows past K are zero (prep passes)
+    auto issue = [&](int c) {
+        const int buf = c % kRst;
+        for (int e = tid; e < kRkc * MT / 4; e += 256) {
+            const int qq = e / (MT / 4), i4 = e - qq * (MT / 4);
+            cp16_rse(&As[buf][qq][4 * i4], At + (int64_t)(c * kRkc + qq) * lda + i_base + 4 * i4);
+        }
+        for (int e = tid; e < kRkc * NT / 4; e += 256) {
+            const int qq = e / (NT / 4), p4 = e - qq * (NT / 4);
+            cp16_rse(&Bs[buf][qq][4 * p4], St + (int64_t)(c * kRkc + qq) * ldb + p_base + 4 * p4);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float acc[TM][8];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int c = 0; c < kRst - 1; ++c) {
+        if (c < nch) issue(c);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRst - 2) : "memory");
+        __syncthreads();  // chunk c landed for everyone; chunk c - 1's buffer is free
+        if (c + kRst - 1 < nch) issue(c + kRst - 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        const int buf = c % kRst;
+        // fragments of step qq + 1 are loaded before the FFMAs of step qq (two register sets)
+        float4 fa[2][TM / 4], fb[2][2];
+        auto frag = [&](int qq, int h) {
+#pragma unroll
+            for (int i = 0; i < TM / 4; ++i) fa[h][i] = *reinterpret_cast<const float4*>(&As[buf][qq][TM * ty + 4 * i]);
+            fb[h][0] = *reinterpret_cast<const float4*>(&Bs[buf][qq][4 * tx]);
+            fb[h][1] = *reinterpret_cast<const float4*>(&Bs[buf][qq][64 + 4 * tx]);
+        };
+        frag(0, 0);
+#pragma unroll
+        for (int qq = 0; qq < kRkc; ++qq) {
+            const int h = qq & 1;
+            if (qq + 1 < kRkc) frag(qq + 1, h ^ 1);
+            float av[TM], bv[8];
+#pragma unroll
+            for (int i = 0; i < TM / 4; ++i) {
+                av[4 * i] = fa[h][i].x;
+                av[4 * i + 1] = fa[h][i].y;
+                av[4 * i + 2] = fa[h][i].z;
+                av[4 * i + 3] = fa[h][i].w;
+            }
+            bv[0] = fb[h][0].x; bv[1] = fb[h][0].y; bv[2] = fb[h][0].z; bv[3] = fb[h][0].w;
+            bv[4] = fb[h][1].x; bv[5] = fb[h][1].y; bv[6] = fb[h][1].z; bv[7] = fb[h][1].w;
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+    }
+    // epilogue: this thread's TM rows of a column are contiguous in X (first index fastest): 16-byte
+    // loads when I0 % 4 == 0. Columns 4 tx + j (j < 4) and 64 + 4 tx + j (the B fragments above).
+    double se = 0.0, sx = 0.0;
+    const bool vec = (I0 & 3) == 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int64_t pc = p_base + (j < 4 ? 4 * tx + j : 64 + 4 * tx + (j - 4));
+        if (pc >= P) continue;
+#pragma unroll
+        for (int i = 0; i < TM; i += 4) {
+            const int64_t i0 = i_base + TM * ty + i;
+            float xv[4];
+            if (vec && i0 + 3 < I0) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(x + i0 + I0 * pc));
+                xv[0] = v.x;
+                xv[1] = v.y;
+                xv[2] = v.z;
+                xv[3] = v.w;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u] = i0 + u < I0 ? x[i0 + u + I0 * pc] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (i0 + u >= I0) continue;
+                const double xd = (double)xv[u];
+                const double d = xd - (double)acc[i + u][j];
+                se = fma(d, d, se);
+                sx = fma(xd, xd, sx);
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        se += __shfl_xor_sync(0xffffffffu, se, o);
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // every warp is past the ring
+    if ((tid & 31) == 0) {
+        red[tid >> 5] = se;
+        red[8 + (tid >> 5)] = sx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a0 += red[w];
+            a1 += red[8 + w];
+        }
+        const int64_t bid = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        block_sums[2 * bid] = a0;
+        block_sums[2 * bid + 1] = a1;
+    }
+}
+
 __global__ void k_sum_pairs(const double* __restrict__ bs, int n, double* out) {
     __shared__ double r0[256], r1[256];
     double a = 0.0, b = 0.0;
@@ -248,8 +424,15 @@ void launch_chain(const double* a, int64_t ra, int64_t p, int64_t rb, const doub
 
 void plan_recon(ReconPlan& p, int) {
     p.threads = 256;
-    p.grid_x = (int)((p.P + PT - 1) / PT);
-    p.grid_y = (int)((p.I0 + RT - 1) / RT);
+    if (p.dtype == F32 && p.write_mode == 0) {  // fp32 RSE: k_rse_f32, 128 columns x 64 (128) rows
+        static const bool t128 = getenv("TRG_RSE_MT128") != nullptr;
+        const int mt = (p.I0 <= 64 || !t128) ? 64 : 128;
+        p.grid_x = (int)((p.P + 127) / 128);
+        p.grid_y = (int)((p.I0 + mt - 1) / mt);
+    } else {
+        p.grid_x = (int)((p.P + PT - 1) / PT);
+        p.grid_y = (int)((p.I0 + RT - 1) / RT);
+    }
     p.nblocks = p.grid_x * p.grid_y;
     p.smem = 0;
 }
@@ -265,8 +448,28 @@ void launch_recon(const ReconPlan& p, const double* g0, const double* S, void* x
     } else {
         if (write_mode)
             k_recon<float, true><<<grid, 256, 0, s>>>(g0, S, (float*)x, p.I0, p.P, p.R0, p.R1, block_sums);
-        else
+        else if (p.write_mode == 2)  // fp64 arithmetic on the fp32 tensor
             k_recon<float, false><<<grid, 256, 0, s>>>(g0, S, (float*)x, p.I0, p.P, p.R0, p.R1, block_sums);
+        else {
+            // K-major fp32 operands, padded to whole tiles: At (K16 x I0 tiles), St (K16 x P tiles)
+            const int K = (int)(p.R0 * p.R1), K16 = (K + kRkc - 1) / kRkc * kRkc;
+            static const bool t128 = getenv("TRG_RSE_MT128") != nullptr;  // development comparison
+            const int mt = (p.I0 <= 64 || !t128) ? 64 : 128;
+            const int64_t lda = (int64_t)p.grid_y * mt, ldb = (int64_t)p.grid_x * 128;
+            float* At = (float*)scratch_alloc(sizeof(float) * (size_t)K16 * lda, s);
+            float* St = (float*)scratch_alloc(sizeof(float) * (size_t)K16 * ldb, s);
+            cudaMemsetAsync(At, 0, sizeof(float) * (size_t)K16 * lda, s);
+            cudaMemsetAsync(St + (size_t)K * ldb, 0, sizeof(float) * (size_t)(K16 - K) * ldb, s);
+            k_rse_prep_a<<<grid_for((int64_t)K * lda), 256, 0, s>>>(g0, p.I0, (int)p.R0, (int)p.R1, lda, At);
+            k_rse_prep_s<<<dim3((unsigned)((ldb + 31) / 32), (unsigned)((K + 31) / 32)), dim3(32, 8), 0, s>>>(
+                S, p.P, (int)p.R0, (int)p.R1, ldb, St);
+            if (mt == 64)
+                k_rse_f32<64><<<grid, 256, 0, s>>>(At, lda, St, ldb, (const float*)x, p.I0, p.P, K, block_sums);
+            else
+                k_rse_f32<128><<<grid, 256, 0, s>>>(At, lda, St, ldb, (const float*)x, p.I0, p.P, K, block_sums);
+            scratch_free(St, s);
+            scratch_free(At, s);
+        }
     }
 }
 

@@ -228,6 +228,8 @@ def test_back_project_parity(trg, ctx):
     ([200, 31], [5, 3], np.float64),
     ([40, 30, 20], [3, 4, 2], np.float32),
     ([9, 8, 7, 6, 5], [2, 2, 3, 2, 2], np.float64),
+    ([150, 30, 20], [3, 4, 2], np.float32),      # I0 > 128: two 128-row tiles of k_rse_f32
+    ([12, 10, 9, 8, 7], [2, 2, 3, 2, 2], np.float32),  # order 5, I0 <= 64 tile
 ])
 def test_rse_parity(trg, dims, ranks, dtype):
     x = tr_tensor(dims, ranks, 12, snr=20.0).astype(dtype)
@@ -235,6 +237,18 @@ def test_rse_parity(trg, dims, ranks, dtype):
     want = orc.rse(x.astype(np.float64), orc.reconstruct_full(cores))
     got = trg.rse(x, cores)
     assert abs(got - want) <= (F64_TOL if dtype == np.float64 else F32_TOL) * want
+
+
+def test_rse_f32_small_error_uses_fp64(trg):
+    """An fp32 fit below RSE 1e-2 is re-measured in fp64 arithmetic (the fp32 GEMM's ~1e-6 relative
+    error on Xhat would otherwise dominate a 1e-4-relative bound on a 1e-4 RSE)."""
+    dims, ranks = [40, 30, 20], [3, 4, 2]
+    cores = orc.random_factors(dims, ranks, 5)
+    xf = orc.add_noise(orc.reconstruct_full(cores), 80.0, 6).astype(np.float32)
+    want = orc.rse(xf.astype(np.float64), orc.reconstruct_full(cores))
+    assert want < 1e-2
+    got = trg.rse(xf, cores)
+    assert abs(got - want) <= F32_TOL * want
 
 
 def test_rse_zero_reference_is_error(trg):
