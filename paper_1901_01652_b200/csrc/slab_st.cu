@@ -338,8 +338,8 @@ struct StSkArgs {
     FastDiv div_npr, div_rb;  // Box-Muller pairs per column run; RB
 };
 
-template <int KG, int D>
-__global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_constant__ CUtensorMap pmap, StSkArgs a) {
+template <int KG, int D, int NC>
+__global__ void __launch_bounds__(NC + 32, 1) k_st_sketch(const __grid_constant__ CUtensorMap pmap, StSkArgs a) {
     constexpr int KQ = KG / 4;
     constexpr int kOR = 3;  // test-matrix ring: item n + 2 is generated while item n is multiplied
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -355,16 +355,16 @@ __global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_cons
     if (tid == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kStCons / 32);
+            mbar_init(&empty[s], NC / 32);
         }
         for (int s = 0; s < kOR; ++s) {
-            mbar_init(&ofull[s], kStCons / 32);
-            mbar_init(&oempty[s], kStCons / 32);
+            mbar_init(&ofull[s], NC / 32);
+            mbar_init(&oempty[s], NC / 32);
         }
         fence_mbar_init();
     }
     __syncthreads();
-    if (warp == kStCons / 32) {  // producer
+    if (warp == NC / 32) {  // producer
         griddep_wait();
         if (lane == 0) {
             const uint64_t pol = policy_l2(0);
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_cons
         const int lb = (int)(it - rbk * a.nlb);
         float* O = om + (size_t)(n % kOR) * a.om_floats;
         const int l0 = lb * a.LB;
-        gen_runs(tid, kStCons, KG * a.RB, a.LB, a.div_npr, a.seed,
+        gen_runs(tid, NC, KG * a.RB, a.LB, a.div_npr, a.seed,
                  [&](int q) {
                      const int k = (int)a.div_rb.div((uint32_t)q), rl = q - k * a.RB;
                      const int64_t r = rbk * a.RB + rl;
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_cons
         }
     }
     // (rs, lq) partial sums -> this CTA's fp64 partial of (d-chunk, k-group), fixed order
-    named_sync(1, kStCons);  // every consumer is past the ring: its memory is free
+    named_sync(1, NC);  // every consumer is past the ring: its memory is free
     float* red = stg;        // [RS * NLQ][DC][KG]
     if (active)
 #pragma unroll
@@ -478,10 +478,10 @@ __global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_cons
 #pragma unroll
                 for (int j = 0; j < KG; ++j) red[((size_t)(rs * a.NLQ + lq) * a.DC + d) * KG + j] = acc[i][j];
         }
-    named_sync(1, kStCons);
+    named_sync(1, NC);
     double* part = a.partial + (int64_t)blockIdx.x * a.dim * a.K;
     const int ngrp = a.RS * a.NLQ;
-    for (int e = tid; e < a.DC * KG; e += kStCons) {
+    for (int e = tid; e < a.DC * KG; e += NC) {
         const int d = e / KG, j = e - d * KG;
         if (d0 + d >= a.dim || k0 + j >= a.K) continue;
         double sum = 0.0;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kStCons + 32, 1) k_st_sketch(const __grid_cons
 }
 
 struct StSkPlan {
-    int KG, ngroups, D, LB, DC, nz, NLQ, NDL, RS, RB, stages, ompitch, npmax;
+    int KG, ngroups, D, LB, DC, nz, NLQ, NDL, RS, RB, stages, ompitch, npmax, NC;
     int64_t nlb, nitems;
     uint32_t p_floats, stage_floats, om_floats;
     size_t smem;
@@ -508,15 +508,17 @@ bool plan_st_sketch(int64_t left, int64_t dim, int K, int64_t right, int num_sms
     p.KG = (K + 3) & ~3;
     p.ngroups = 1;
     p.D = p.KG <= 16 ? 4 : 3;
+    // 16 consumer warps when the accumulators leave the registers for them (KG <= 12: C5), else 8
+    p.NC = p.KG <= 12 ? 512 : kStCons;
     // whole rows of l when short (TMA rows of >= 48 bytes), else 64-wide blocks
     p.LB = left <= 64 ? (int)left : pick_lb(left, 64);
     p.NLQ = p.LB / 4;
-    if (p.NLQ > kStCons) return false;
-    p.NDL = (int)std::min<int64_t>({(dim + p.D - 1) / p.D, (int64_t)kStCons / p.NLQ, (int64_t)256 / p.D});
+    if (p.NLQ > p.NC) return false;
+    p.NDL = (int)std::min<int64_t>({(dim + p.D - 1) / p.D, (int64_t)p.NC / p.NLQ, (int64_t)256 / p.D});
     p.DC = (int)std::min<int64_t>(dim, (int64_t)p.NDL * p.D);  // <= 256: a TMA box dimension
     p.NDL = (p.DC + p.D - 1) / p.D;
     p.nz = (int)((dim + p.DC - 1) / p.DC);
-    p.RS = std::max(1, kStCons / (p.NLQ * p.NDL));
+    p.RS = std::max(1, p.NC / (p.NLQ * p.NDL));
     // RB: a multiple of RS with ~16-32 KB of P per stage
     const int64_t slab = (int64_t)p.DC * p.LB;  // floats per slab of the box
     int64_t rb = std::max<int64_t>(p.RS, (16 * 1024 / 4 + slab - 1) / slab);
@@ -781,18 +783,18 @@ int launch_st_sketch(const SketchPlan& sp, const void* x, double* partial, doubl
     a.col_off = sp.col_off;
     a.div_npr = FastDiv((uint32_t)(p.LB / 2 + 1));
     a.div_rb = FastDiv((uint32_t)p.RB);
-    const dim3 grid(p.gx, p.ngroups, p.nz), block(kStCons + 32);
-#define TRG_STSK(KGV, DV)                                               \
-    do {                                                                \
-        allow_smem(k_st_sketch<KGV, DV>, p.smem);                       \
-        pdl_launch(k_st_sketch<KGV, DV>, grid, block, p.smem, s, map, a); \
+    const dim3 grid(p.gx, p.ngroups, p.nz), block(p.NC + 32);
+#define TRG_STSK(KGV, DV, NCV)                                               \
+    do {                                                                     \
+        allow_smem(k_st_sketch<KGV, DV, NCV>, p.smem);                       \
+        pdl_launch(k_st_sketch<KGV, DV, NCV>, grid, block, p.smem, s, map, a); \
     } while (0)
     switch (p.KG) {
-        case 4: TRG_STSK(4, 4); break;
-        case 8: TRG_STSK(8, 4); break;
-        case 12: TRG_STSK(12, 4); break;
-        case 16: TRG_STSK(16, 4); break;
-        default: TRG_STSK(20, 3); break;
+        case 4: TRG_STSK(4, 4, 512); break;
+        case 8: TRG_STSK(8, 4, 512); break;
+        case 12: TRG_STSK(12, 4, 512); break;
+        case 16: TRG_STSK(16, 4, kStCons); break;
+        default: TRG_STSK(20, 3, kStCons); break;
     }
 #undef TRG_STSK
     if (y) launch_reduce_partials(partial, p.gx, sp.dim * sp.K, y, s);
