@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 def _flags():
     return ARCH + [
         "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-        "-Xcompiler", "-fPIC,-fopenmp,-O3",
+        "-Xcompiler", "-fPIC,-fopenmp,-O3,-march=x86-64-v4",
         "-Xptxas", "-v" if os.environ.get("TRG_PTXAS_VERBOSE") else "-O3",
         "-ccbin", "g++",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,

@@ -10,6 +10,10 @@
 #include <omp.h>
 
 #include "random_host.hpp"
+#include <chrono>
+#include <cstdio>
+double g_t[6];
+static double nowms(){return std::chrono::duration<double,std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();}
 
 namespace trg {
 namespace host {
@@ -663,8 +667,14 @@ void als_update_mode(const Mat& xn_tr, Cores& f, idx n) {
     const idx m = f.rank(n) * f.rank((n + 1) % f.order());
     Mat z;
     if (n_cols <= kDirectLsMaxRows && n_cols >= m) {
+        double t0 = nowms();
         const Tensor s = subchain(f, n);
-        z = ls_solve_qr(unfold_tr(s, 1), transpose(xn_tr));
+        double t1 = nowms();
+        Mat A = unfold_tr(s, 1); Mat B = transpose(xn_tr);
+        double t2 = nowms();
+        z = ls_solve_qr(A, B);
+        double t3 = nowms();
+        g_t[0] += t1 - t0; g_t[1] += t2 - t1; g_t[2] += t3 - t2;
     } else {
         z = ls_solve_gram(subchain_gram(f, n), transpose(subchain_rhs(xn_tr, f, n)));
     }
@@ -886,7 +896,9 @@ SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance,
     SolveOut o;
     for (idx sweep = 1; sweep <= max_sweeps; ++sweep) {
         for (idx n = 0; n < N; ++n) als_update_mode(unf[static_cast<size_t>(n)], f, n);
+        double t4 = nowms();
         o.rse_history.push_back(rse(x, reconstruct_full(f)));
+        g_t[3] += nowms() - t4;
         o.sweeps_run = sweep;
         const size_t k = o.rse_history.size();
         if (k >= 2 && std::abs(o.rse_history[k - 1] - o.rse_history[k - 2]) < tolerance * o.rse_history[k - 2]) break;

@@ -10,6 +10,10 @@
 #include <omp.h>
 
 #include "random_host.hpp"
+#include <chrono>
+#include <cstdio>
+double g_t[6];
+static double nowms(){return std::chrono::duration<double,std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();}
 
 namespace trg {
 namespace host {
@@ -47,15 +51,9 @@ Split split(const std::vector<idx>& s, idx mode) {
 Mat unfold_tr(const Tensor& t, idx mode) {
     const Split s = split(t.shape, mode);
     Mat m(s.dim, s.left * s.right);
-    // d in blocks of 64: the block's left x 64 source elements stay in L1 across the l loop
-    constexpr idx DB = 64;
-    const idx nblk = (s.dim + DB - 1) / DB;
-#pragma omp parallel for collapse(2) schedule(static) if (t.size() > (1 << 16))
-    for (idx r = 0; r < s.right; ++r)
-        for (idx b = 0; b < nblk; ++b)
-            for (idx l = 0; l < s.left; ++l)
-                for (idx d = b * DB; d < std::min(s.dim, (b + 1) * DB); ++d)
-                    m(d, r + s.right * l) = t.data[static_cast<size_t>(l + s.left * (d + s.dim * r))];
+    for (idx l = 0; l < s.left; ++l)
+        for (idx r = 0; r < s.right; ++r)
+            for (idx d = 0; d < s.dim; ++d) m(d, r + s.right * l) = t.data[static_cast<size_t>(l + s.left * (d + s.dim * r))];
     return m;
 }
 
@@ -69,15 +67,10 @@ Mat core_unfold1(const Tensor& g) {
     return m;
 }
 
-// 32 x 32 blocks: both the reads and the writes stay within a few cache lines / pages per block
 Mat transpose(const Mat& m) {
     Mat t(m.c, m.r);
-    constexpr idx B = 32;
-#pragma omp parallel for schedule(static) if (m.r * m.c > (1 << 16))
-    for (idx j0 = 0; j0 < m.c; j0 += B)
-        for (idx i0 = 0; i0 < m.r; i0 += B)
-            for (idx j = j0; j < std::min(m.c, j0 + B); ++j)
-                for (idx i = i0; i < std::min(m.r, i0 + B); ++i) t(j, i) = m(i, j);
+    for (idx j = 0; j < m.c; ++j)
+        for (idx i = 0; i < m.r; ++i) t(j, i) = m(i, j);
     return t;
 }
 
@@ -297,7 +290,6 @@ struct HQR {
                 double* cj = qr.col(j);
                 const idx lo = j + 1 + (m - j - 1) * th / nt, hi = j + 1 + (m - j - 1) * (th + 1) / nt;
                 double tl = 0.0;
-#pragma omp simd reduction(+ : tl)
                 for (idx i = lo; i < hi; ++i) tl += cj[i] * cj[i];
                 part[(size_t)th * (kPanelNb + 1)] = tl;
 #pragma omp barrier
@@ -325,7 +317,6 @@ struct HQR {
                 if (t == 0.0) {
                     for (idx i = lo; i < hi; ++i) cj[i] = 0.0;
                 } else {
-#pragma omp simd
                     for (idx i = lo; i < hi; ++i) cj[i] *= inv;
                 }
                 const idx ncols = j0 + nb - j - 1;
@@ -334,7 +325,6 @@ struct HQR {
                     for (idx c = 0; c < ncols; ++c) {
                         const double* cc = qr.col(j + 1 + c);
                         double w = 0.0;
-#pragma omp simd reduction(+ : w)
                         for (idx i = lo; i < hi; ++i) w += cj[i] * cc[i];
                         pp[c] = w;
                     }
@@ -350,7 +340,6 @@ struct HQR {
                     for (idx c = 0; c < ncols; ++c) {
                         double* cc = qr.col(j + 1 + c);
                         const double w = shared[3 + c];
-#pragma omp simd
                         for (idx i = lo; i < hi; ++i) cc[i] -= w * cj[i];
                     }
                 }
@@ -362,7 +351,9 @@ struct HQR {
         const idx m = qr.r, n = qr.c, k = std::min(m, n);
         for (idx j0 = 0; j0 < k; j0 += kNb) {
             const idx nb = std::min(kNb, k - j0);
+            double t0 = nowms();
             factor_panel(j0, nb);
+            double t1 = nowms(); g_t[0] += t1 - t0;
             // T: T(0:p, p) = -tau_p T(0:p, 0:p) V(:, 0:p)^T v_p, T(p, p) = tau_p, with V^T V of the panel
             // (rows >= j0 + p of v_q against v_p) from one row-parallel pass in a fixed order
             const int nt = std::max(1, std::min(omp_get_max_threads(), (int)((m - j0) / 512)));
@@ -402,6 +393,7 @@ struct HQR {
                 }
                 T[static_cast<size_t>(p + nb * p)] = tp;
             }
+            double t2 = nowms(); g_t[1] += t2 - t1;
             const double* Tp = T.data();
             const idx c0 = j0 + nb, nchunk = (n - c0 + 3) / 4;
 #pragma omp parallel for schedule(dynamic, 1)
@@ -409,6 +401,7 @@ struct HQR {
                 const idx c = c0 + 4 * ch;
                 panel_apply4(qr.a.data(), m, m, j0, nb, Tp, qr.col(c), m, std::min<idx>(4, n - c));
             }
+            g_t[2] += nowms() - t2;
             Ts.push_back(std::move(T));
         }
     }
@@ -442,21 +435,16 @@ struct HQR {
         }
         return back_substitute(y, b.c);
     }
-    // R x = y column by column of R (contiguous), bottom up: x_j = y_j / R_jj, then y(0:j) -= x_j R(0:j, j)
     Mat back_substitute(const Mat& y, idx nc) const {
         const idx n = qr.c;
         Mat x(n, nc);
 #pragma omp parallel for schedule(static) if (nc * n * n > (1 << 16))
-        for (idx c = 0; c < nc; ++c) {
-            std::vector<double> t(y.col(c), y.col(c) + n);
-            for (idx j = n - 1; j >= 0; --j) {
-                const double xj = t[static_cast<size_t>(j)] / qr(j, j);
-                x(j, c) = xj;
-                const double* rj = qr.col(j);
-#pragma omp simd
-                for (idx i = 0; i < j; ++i) t[static_cast<size_t>(i)] -= xj * rj[i];
+        for (idx c = 0; c < nc; ++c)
+            for (idx i = n - 1; i >= 0; --i) {
+                double s = y(i, c);
+                for (idx j = i + 1; j < n; ++j) s -= qr(i, j) * x(j, c);
+                x(i, c) = s / qr(i, i);
             }
-        }
         return x;
     }
 };
@@ -554,14 +542,17 @@ Mat ridge_solve(Mat gram, const Mat& rhs) {
 // solvers.hpp:195-205
 Mat ls_solve_qr(const Mat& a, const Mat& b) {
     if (a.r >= a.c) {
+        double ta = nowms();
         HQR qr(a);
+        g_t[3] += nowms() - ta;
         double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
         for (idx i = 0; i < a.c; ++i) {
             dmax = std::max(dmax, std::abs(qr.qr(i, i)));
             dmin = std::min(dmin, std::abs(qr.qr(i, i)));
         }
         const double cutoff = dmax * static_cast<double>(std::max(a.r, a.c)) * std::numeric_limits<double>::epsilon() * 16.0;
-        if (dmax > 0.0 && dmin > cutoff) return qr.solve(b);
+        double tb = nowms();
+        if (dmax > 0.0 && dmin > cutoff) { Mat r = qr.solve(b); g_t[4] += nowms() - tb; return r; }
     }
     return ridge_solve(matmul_tn(a, a), matmul_tn(a, b));
 }
