@@ -8,7 +8,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrg.so")
+LIB_PATH = os.environ.get("TRG_LIB_PATH") or os.path.join(HERE, "libtrg.so")  # override: A/B builds (development)
 
 c_i64p = ctypes.POINTER(ctypes.c_int64)
 c_dp = ctypes.POINTER(ctypes.c_double)
