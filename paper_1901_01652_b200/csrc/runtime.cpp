@@ -780,12 +780,13 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     if (!sk->ev0) CK(cudaEventCreate(&sk->ev0));
     if (!sk->ev1) CK(cudaEventCreate(&sk->ev1));
     CK(cudaEventRecord(sk->ev0, ctx->stream));
-    sk->dflags = (int*)ctx->alloc(sizeof(int) * 3 * N);  // + N arrival tickets of the fused QR reduce
+    const int nflags = 3 * N;  // QR path flags, N arrival tickets of the fused QR reduce
+    sk->dflags = (int*)ctx->alloc(sizeof(int) * nflags);
     static const bool memset_flags = getenv("TRG_FLAGS_MEMSET") != nullptr;  // development switch
     if (memset_flags) {
-        CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * 3 * N, ctx->stream));
+        CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * nflags, ctx->stream));
     } else {
-        trg::launch_zero_ints(sk->dflags, 3 * N, ctx->stream);
+        trg::launch_zero_ints(sk->dflags, nflags, ctx->stream);
         ctx->launches += 1;
     }
     const KrPlan krp = kr_on ? build_kr(ctx, x, Kin, seed, variant) : KrPlan{};
