@@ -282,46 +282,44 @@ struct HQR {
         }
     }
     // One panel: reflectors of columns j0 .. j0 + nb (Eigen's makeHouseholder, as HQR's unblocked
-    // loop), the panel columns updated as they go. Row-parallel inside one OpenMP region: per
-    // column, one fixed-order reduction for the tail norm and one for the dot products with the
-    // rest of the panel; the reduced values are computed once and read by every thread.
+    // loop), the panel columns updated as they go. Row-parallel inside one OpenMP region with a fixed
+    // row partition of [j0, m) (fixed-order reductions, bit-reproducible for a given thread count) and
+    // two barriers per column: every thread derives beta / tau from the tail-norm partials itself,
+    // the reflector's unit entry at row j is folded into the dot products of its owner (v_j(j) = 1),
+    // and each thread's axpy pass also forms its partial of the next column's tail norm.
     void factor_panel(idx j0, idx nb) {
         const idx m = qr.r;
         const int nt = std::max(1, std::min(omp_get_max_threads(), (int)((m - j0) / 256)));
-        std::vector<double> part((size_t)nt * (kPanelNb + 1), 0.0);
-        std::vector<double> shared(kPanelNb + 3, 0.0);  // [0] tail, [1] t, [2] inv, [3..] w
+        std::vector<double> ptail((size_t)nt, 0.0), pdot((size_t)nt * kPanelNb, 0.0);
 #pragma omp parallel num_threads(nt)
         {
             const int th = omp_get_thread_num();
-            for (idx j = j0; j < j0 + nb; ++j) {
-                double* cj = qr.col(j);
-                const idx lo = j + 1 + (m - j - 1) * th / nt, hi = j + 1 + (m - j - 1) * (th + 1) / nt;
+            const idx flo = j0 + (m - j0) * th / nt, fhi = j0 + (m - j0) * (th + 1) / nt;
+            {
+                const double* c = qr.col(j0);
                 double tl = 0.0;
 #pragma omp simd reduction(+ : tl)
-                for (idx i = lo; i < hi; ++i) tl += cj[i] * cj[i];
-                part[(size_t)th * (kPanelNb + 1)] = tl;
+                for (idx i = std::max(flo, j0 + 1); i < fhi; ++i) tl += c[i] * c[i];
+                ptail[(size_t)th] = tl;
+            }
 #pragma omp barrier
-#pragma omp single
-                {
-                    double tail = 0.0;
-                    for (int t2 = 0; t2 < nt; ++t2) tail += part[(size_t)t2 * (kPanelNb + 1)];
-                    const double c0 = cj[j];
-                    double beta, t, inv = 0.0;
-                    if (tail <= std::numeric_limits<double>::min()) {  // Eigen makeHouseholder
-                        t = 0.0;
-                        beta = c0;
-                    } else {
-                        beta = std::sqrt(c0 * c0 + tail);
-                        if (c0 >= 0.0) beta = -beta;
-                        inv = 1.0 / (c0 - beta);
-                        t = (beta - c0) / beta;
-                    }
-                    cj[j] = beta;
-                    tau[static_cast<size_t>(j)] = t;
-                    shared[1] = t;
-                    shared[2] = inv;
-                }  // implicit barrier
-                const double t = shared[1], inv = shared[2];
+            for (idx j = j0; j < j0 + nb; ++j) {
+                double* cj = qr.col(j);
+                double tail = 0.0;
+                for (int t2 = 0; t2 < nt; ++t2) tail += ptail[(size_t)t2];
+                const double c0 = cj[j];  // row j: last written before the previous barrier
+                double beta, t, inv = 0.0;
+                if (tail <= std::numeric_limits<double>::min()) {  // Eigen makeHouseholder
+                    t = 0.0;
+                    beta = c0;
+                } else {
+                    beta = std::sqrt(c0 * c0 + tail);
+                    if (c0 >= 0.0) beta = -beta;
+                    inv = 1.0 / (c0 - beta);
+                    t = (beta - c0) / beta;
+                }
+                const idx lo = std::max(flo, j + 1), hi = fhi;
+                const bool own_j = flo <= j && j < fhi;
                 if (t == 0.0) {
                     for (idx i = lo; i < hi; ++i) cj[i] = 0.0;
                 } else {
@@ -329,31 +327,36 @@ struct HQR {
                     for (idx i = lo; i < hi; ++i) cj[i] *= inv;
                 }
                 const idx ncols = j0 + nb - j - 1;
-                if (t != 0.0 && ncols > 0) {
-                    double* pp = part.data() + (size_t)th * (kPanelNb + 1);
+                double* pp = pdot.data() + (size_t)th * kPanelNb;
+                if (t != 0.0)
                     for (idx c = 0; c < ncols; ++c) {
                         const double* cc = qr.col(j + 1 + c);
-                        double w = 0.0;
+                        double w = own_j ? cc[j] : 0.0;  // v_j(j) = 1
 #pragma omp simd reduction(+ : w)
                         for (idx i = lo; i < hi; ++i) w += cj[i] * cc[i];
                         pp[c] = w;
                     }
 #pragma omp barrier
-#pragma omp single
-                    for (idx c = 0; c < ncols; ++c) {
-                        double w = qr.col(j + 1 + c)[j];  // unit diagonal
-                        for (int t2 = 0; t2 < nt; ++t2) w += part[(size_t)t2 * (kPanelNb + 1) + c];
+                if (th == 0) tau[static_cast<size_t>(j)] = t;
+                if (own_j) cj[j] = beta;
+                double tl = 0.0;
+                for (idx c = 0; c < ncols; ++c) {
+                    double* cc = qr.col(j + 1 + c);
+                    if (t != 0.0) {
+                        double w = 0.0;
+                        for (int t2 = 0; t2 < nt; ++t2) w += pdot[(size_t)t2 * kPanelNb + c];
                         w *= t;
-                        qr.col(j + 1 + c)[j] -= w;
-                        shared[3 + c] = w;
-                    }  // implicit barrier
-                    for (idx c = 0; c < ncols; ++c) {
-                        double* cc = qr.col(j + 1 + c);
-                        const double w = shared[3 + c];
+                        if (own_j) cc[j] -= w;
 #pragma omp simd
                         for (idx i = lo; i < hi; ++i) cc[i] -= w * cj[i];
                     }
+                    if (c == 0) {  // the next column's tail-norm partial (rows > j + 1)
+                        const idx l2 = std::max(flo, j + 2);
+#pragma omp simd reduction(+ : tl)
+                        for (idx i = l2; i < hi; ++i) tl += cc[i] * cc[i];
+                    }
                 }
+                ptail[(size_t)th] = tl;
 #pragma omp barrier
             }
         }

@@ -133,6 +133,163 @@ __global__ void __launch_bounds__(256) k_recon(const double* __restrict__ g0, co
 }
 
 
+// ---- K8 / K9 on the FP64 tensor pipe (m8n8k4 DMMA): Xhat(i0, p) = sum_q A(i0, q) B(q, p) with
+// q = b + R1 a, A(i0, q) = G0(a, i0, b) and B(q, p) = S(b, p, a) (tr_factors.hpp:123-137), for
+// K = R0 R1 <= 64. CTA = (a block of up to 128 rows of i0, a persistent loop over 64-column tiles of
+// p): A lives in shared memory for the whole launch, the B tile of the next columns streams in by
+// cp.async while the current one is multiplied. Warp job = (8-row tile, two 8-column tiles) over
+// all of K; the epilogue reads X straight into the accumulator layout and forms sum (x - xhat)^2
+// and sum x^2 (solvers.hpp:47-54), or writes Xhat (synthesis). A tile's columns are a fixed set
+// and the CTA's sums run in a fixed order: bit-reproducible.
+constexpr int kRdCols = 64;  // columns of p per tile
+constexpr int kRdMaxRows = 128;
+constexpr int kRdMaxK = 64;
+constexpr int kRdThreads = 512;
+
+__device__ __forceinline__ void rd_dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void rd_cp8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+
+template <typename T, bool WRITE>
+__global__ void __launch_bounds__(kRdThreads, 1)
+    k_recon_dmma(const double* __restrict__ g0, const double* __restrict__ S, T* x, int64_t I0, int64_t P, int R0, int R1,
+                 int Kp, int ldg, int lds, double* __restrict__ block_sums) {
+    extern __shared__ __align__(16) double rd_smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int K = R0 * R1;
+    const int64_t row0 = (int64_t)blockIdx.y * kRdMaxRows;
+    const int rows = (int)min((int64_t)kRdMaxRows, I0 - row0);
+    const int mtiles = (rows + 7) / 8;
+    double* Gs = rd_smem;                                   // [mtiles * 8][ldg]
+    double* Ss = Gs + (size_t)mtiles * 8 * ldg;             // [2][Kp][lds]
+    double* red = Ss + 2 * (size_t)Kp * lds;                // [2][16]
+    // A = G0 rows of this block, zero-padded to whole tiles and to Kp
+    for (int e = tid; e < mtiles * 8 * Kp; e += kRdThreads) {
+        const int r = e / Kp, q = e - r * Kp;
+        double v = 0.0;
+        if (r < rows && q < K) {
+            const int a = q / R1, b = q - a * R1;
+            v = g0[a + (int64_t)R0 * ((row0 + r) + I0 * b)];
+        }
+        Gs[r * ldg + q] = v;
+    }
+    const int64_t ntiles = (P + kRdCols - 1) / kRdCols;
+    // B(q, p) = S[b + R1 (p + P a)]: for each a, R1 x 64 consecutive doubles (b fastest)
+    auto issue = [&](int64_t t, int buf) {
+        const int64_t p0 = t * kRdCols;
+        const int pc = (int)min((int64_t)kRdCols, P - p0);
+        double* dst = Ss + (size_t)buf * Kp * lds;
+        for (int e = tid; e < K * kRdCols; e += kRdThreads) {
+            const int a = e / (R1 * kRdCols), rem = e - a * (R1 * kRdCols);
+            const int pp = rem / R1, b = rem - pp * R1;
+            if (pp < pc) rd_cp8(dst + (b + R1 * a) * lds + pp, S + b + (int64_t)R1 * (p0 + pp + P * a));
+            else dst[(b + R1 * a) * lds + pp] = 0.0;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // padded rows q in [K, Kp) of both buffers stay zero
+    for (int e = tid; e < 2 * (Kp - K) * lds; e += kRdThreads) {
+        const int bq = e / lds, c = e - bq * lds;
+        Ss[(size_t)(bq / (Kp - K)) * Kp * lds + (size_t)(K + bq % (Kp - K)) * lds + c] = 0.0;
+    }
+    double se = 0.0, sx = 0.0;
+    const int njobs = mtiles * (kRdCols / 16);  // (8-row tile, pair of 8-column tiles)
+    int64_t t = blockIdx.x;
+    if (t < ntiles) issue(t, 0);
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const int64_t tn = t + gridDim.x;
+        if (tn < ntiles) {
+            issue(tn, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double* Sb = Ss + (size_t)buf * Kp * lds;
+        const int64_t p0 = t * kRdCols;
+        for (int job = warp; job < njobs; job += kRdThreads / 32) {
+            const int mt = job % mtiles, np = job / mtiles;
+            const int r = 8 * mt + (lane >> 2);  // D fragment row; columns 2 (lane & 3) + {0, 1}
+            // this lane's X entries first (epilogue operands in flight during the MMAs)
+            double xv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            if (!WRITE) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int64_t p = p0 + 8 * (2 * np + h) + 2 * (lane & 3) + c;
+                        if (r < rows && p < P) xv[h][c] = (double)x[(row0 + r) + I0 * p];
+                    }
+            }
+            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            const double* ar = Gs + (8 * mt + (lane >> 2)) * ldg + (lane & 3);
+            const double* br = Sb + (lane & 3) * lds + 16 * np + (lane >> 2);
+#pragma unroll 4
+            for (int ks = 0; ks < Kp / 4; ++ks) {
+                const double av = ar[4 * ks];
+                const double b0 = br[4 * ks * lds], b1 = br[4 * ks * lds + 8];
+                rd_dmma(acc[0][0], acc[0][1], av, b0);
+                rd_dmma(acc[1][0], acc[1][1], av, b1);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int64_t p = p0 + 8 * (2 * np + h) + 2 * (lane & 3) + c;
+                    if (r < rows && p < P) {
+                        if (WRITE) {
+                            x[(row0 + r) + I0 * p] = T(acc[h][c]);
+                        } else {
+                            const double d = xv[h][c] - acc[h][c];
+                            se = fma(d, d, se);
+                            sx = fma(xv[h][c], xv[h][c], sx);
+                        }
+                    }
+                }
+        }
+        __syncthreads();  // the buffer is refilled two tiles later
+    }
+    if (!WRITE) {
+        for (int o = 16; o > 0; o >>= 1) {
+            se += __shfl_xor_sync(0xffffffffu, se, o);
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        }
+        if (lane == 0) {
+            red[warp] = se;
+            red[16 + warp] = sx;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a0 = 0.0, a1 = 0.0;
+            for (int w = 0; w < kRdThreads / 32; ++w) {
+                a0 += red[w];
+                a1 += red[16 + w];
+            }
+            const int64_t bid = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+            block_sums[2 * bid] = a0;
+            block_sums[2 * bid + 1] = a1;
+        }
+    }
+}
+
+bool recon_dmma_ok(const ReconPlan& p) {
+    return !getenv("TRG_RECON_SIMT") && p.R0 * p.R1 <= kRdMaxK && p.I0 >= 1 && p.P >= 1 &&
+           (p.dtype == F64 || p.write_mode != 0);  // fp32 RSE sums: k_rse_f32 (FFMA) unless fp64 is asked for
+}
+
+size_t recon_dmma_smem(int64_t I0, int Kp, int ldg, int lds) {
+    const int64_t rows = std::min<int64_t>(I0, kRdMaxRows);
+    return sizeof(double) * ((size_t)((rows + 7) / 8) * 8 * ldg + 2 * (size_t)Kp * lds + 32);
+}
+
 // ---- K8 for fp32 tensors: Xhat(i0, p) = sum_{a,b} G0(a, i0, b) S(b, p, a) (tr_factors.hpp:123-137) as a
 // register-tiled FFMA GEMM on fp32 operands (the tensor is fp32; the RSE tolerance is 1e-4), with
 // sum (x - xhat)^2 and x^2 accumulated in fp64 in the epilogue (solvers.hpp:47-54). The operands
@@ -422,8 +579,16 @@ void launch_chain(const double* a, int64_t ra, int64_t p, int64_t rb, const doub
     k_chain<<<grid_for(n), 256, 0, s>>>(a, ra, p, rb, g, i, rc, out);
 }
 
-void plan_recon(ReconPlan& p, int) {
+void plan_recon(ReconPlan& p, int num_sms) {
     p.threads = 256;
+    if (recon_dmma_ok(p)) {  // DMMA: persistent column loop, one CTA per SM over the row blocks
+        p.grid_y = (int)((p.I0 + kRdMaxRows - 1) / kRdMaxRows);
+        p.grid_x = (int)std::max<int64_t>(1, std::min<int64_t>((p.P + kRdCols - 1) / kRdCols, num_sms / p.grid_y));
+        p.nblocks = p.grid_x * p.grid_y;
+        p.threads = kRdThreads;
+        p.smem = 0;
+        return;
+    }
     if (p.dtype == F32 && p.write_mode == 0) {  // fp32 RSE: k_rse_f32, 128 columns x 64 (128) rows
         static const bool t128 = getenv("TRG_RSE_MT128") != nullptr;
         const int mt = (p.I0 <= 64 || !t128) ? 64 : 128;
@@ -440,6 +605,26 @@ void plan_recon(ReconPlan& p, int) {
 void launch_recon(const ReconPlan& p, const double* g0, const double* S, void* x, int write_mode, double* block_sums,
                   cudaStream_t s) {
     dim3 grid(p.grid_x, p.grid_y);
+    if (recon_dmma_ok(p)) {
+        const int K = (int)(p.R0 * p.R1), Kp = (K + 3) & ~3;
+        int ldg = Kp;
+        while (ldg % 16 != 4) ++ldg;  // 8 rows x 4 k of an A fragment over all 32 banks
+        const int lds = kRdCols + 8;   // 4 k rows x 8 columns of a B fragment: two conflict-free halves
+        const size_t smem = recon_dmma_smem(p.I0, Kp, ldg, lds);
+        const bool wr = write_mode == 1;
+        auto go = [&](auto kern, auto* xp) {
+            allow_smem(kern, smem);
+            kern<<<grid, kRdThreads, smem, s>>>(g0, S, xp, p.I0, p.P, (int)p.R0, (int)p.R1, Kp, ldg, lds, block_sums);
+        };
+        if (p.dtype == F64) {
+            if (wr) go(k_recon_dmma<double, true>, (double*)x);
+            else go(k_recon_dmma<double, false>, (double*)x);
+        } else {
+            if (wr) go(k_recon_dmma<float, true>, (float*)x);
+            else go(k_recon_dmma<float, false>, (float*)x);
+        }
+        return;
+    }
     if (p.dtype == F64) {
         if (write_mode)
             k_recon<double, true><<<grid, 256, 0, s>>>(g0, S, (double*)x, p.I0, p.P, p.R0, p.R1, block_sums);
