@@ -180,6 +180,20 @@ struct trg_ctx {
     cudaMemPool_t pool = nullptr;  // private stream-ordered pool (release threshold: keep)
     ncclComm_t comm = nullptr;
     trg_loopback* lb = nullptr;  // loopback ranks (no NCCL): see reduce_loopback
+    // arrival tickets of the fused QR reduce, one per mode: zeroed once here, and every QR launch
+    // leaves its ticket at zero again (the last arriving CTA resets it), so a projection needs no
+    // zeroing kernel of its own
+    int* tickets = nullptr;
+    int tickets_n = 0;
+    int* ensure_tickets(int n) {
+        if (n > tickets_n) {
+            if (tickets) cudaFreeAsync(tickets, stream);
+            tickets_n = std::max(n, 16);
+            CK(cudaMallocFromPoolAsync((void**)&tickets, sizeof(int) * tickets_n, pool, stream));
+            CK(cudaMemsetAsync(tickets, 0, sizeof(int) * tickets_n, stream));
+        }
+        return tickets;
+    }
     bool profiling = false;
     int64_t launches = 0;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -330,7 +344,7 @@ struct trg_sketch {
     std::vector<int64_t> dims, K;
     std::vector<double*> dQ;  // device Q_n (nullptr for skipped modes)
     std::vector<double*> dY;  // device Y_n full rows
-    int* dflags = nullptr;    // N QR-path flags, N (unused), N QR-reduce tickets
+    int* dflags = nullptr;    // N QR-path flags
     void* dP = nullptr;       // device P (dtype), full prod K
     bool P_is_view = false;   // P aliases x (no mode projected, unsharded)
     int64_t P_elems = 0;
@@ -780,15 +794,10 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
     if (!sk->ev0) CK(cudaEventCreate(&sk->ev0));
     if (!sk->ev1) CK(cudaEventCreate(&sk->ev1));
     CK(cudaEventRecord(sk->ev0, ctx->stream));
-    const int nflags = 3 * N;  // QR path flags, N arrival tickets of the fused QR reduce
-    sk->dflags = (int*)ctx->alloc(sizeof(int) * nflags);
-    static const bool memset_flags = getenv("TRG_FLAGS_MEMSET") != nullptr;  // development switch
-    if (memset_flags) {
-        CK(cudaMemsetAsync(sk->dflags, 0, sizeof(int) * nflags, ctx->stream));
-    } else {
-        trg::launch_zero_ints(sk->dflags, nflags, ctx->stream);
-        ctx->launches += 1;
-    }
+    // QR path flags, written by every QR launch (skipped modes have none: trg_sketch_qr_path
+    // answers 0 for them without reading the device)
+    sk->dflags = (int*)ctx->alloc(sizeof(int) * N);
+    int* tickets = ctx->ensure_tickets(N);
     const KrPlan krp = kr_on ? build_kr(ctx, x, Kin, seed, variant) : KrPlan{};
     auto krn = [&](int n) { return kr_on ? &krp.om[n] : nullptr; };
     ctx->scr_begin();
@@ -827,7 +836,7 @@ void run_sketch(trg_ctx* ctx, const trg_tensor* x, const int64_t* Kin, uint64_t 
                 }
             ctx->launch("qr", [&] {
                 trg::launch_qr_fused(yparts[n].partial, yparts[n].nparts, In, (int)Kn, sk->dY[n], sk->dQ[n], work,
-                                     sk->dflags + n, sk->dflags + 2 * N + n, ctx->stream, job, ctx->num_sms);
+                                     sk->dflags + n, tickets + n, ctx->stream, job, ctx->num_sms);
             });
             ctx->tmp_free(yparts[n].partial);
             yparts[n] = YParts{};
@@ -1349,6 +1358,7 @@ int trg_ctx_destroy(trg_ctx* ctx) {
         if (ctx->comm) nccl().commDestroy(ctx->comm);
         cudaStreamSynchronize(ctx->side);
         if (ctx->scr_base) cudaFreeAsync(ctx->scr_base, ctx->stream);
+        if (ctx->tickets) cudaFreeAsync(ctx->tickets, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->side);
         cudaStreamDestroy(ctx->stream);
@@ -1542,6 +1552,10 @@ int trg_sketch_qr_path(const trg_sketch* sk, int mode, int* hh) {
     return guard([&] {
             if (mode < 0 || mode >= (int)sk->dims.size()) throw std::out_of_range("mode out of range");
         int v = 0;
+        if (sk->K[mode] == sk->dims[mode]) {  // identity basis: no QR ran (sketch.hpp:76-79)
+            *hh = 0;
+            return;
+        }
         CK(cudaMemcpyAsync(&v, sk->dflags + mode, sizeof(int), cudaMemcpyDeviceToHost, sk->ctx->stream));
         CK(cudaStreamSynchronize(sk->ctx->stream));
         *hh = v;
