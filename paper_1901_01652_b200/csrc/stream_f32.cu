@@ -35,9 +35,13 @@ namespace trg {
 
 namespace {
 
-constexpr int kF32Cons = 8;
+#ifndef TRG_F32_CONS
+#define TRG_F32_CONS 8
+#endif
+constexpr int kF32Cons = TRG_F32_CONS;
 #ifndef TRG_F32_GEN_SMALL
-#define TRG_F32_GEN_SMALL 16  // generator warps when TK <= 12 (dense test-matrix tiles, C5)
+#define TRG_F32_GEN_SMALL 12  // generator warps when TK <= 12 (dense test-matrix tiles, C5): 8 / 12 / 16 measured
+                              // 1037 / 1031 / 1060 us on C5 with the MUFU Box-Muller
 #endif
 #ifndef TRG_F32_GEN_LARGE
 #define TRG_F32_GEN_LARGE 4
@@ -123,7 +127,9 @@ __global__ void __launch_bounds__((kF32Cons + GEN + 1) * 32, 1)
         return;
     }
     if (warp >= kF32Cons) {
-        // ---- generators: Omega(c, k) = draw D + col_off + c + rows_glob k, pairs shared
+        // ---- generators: Omega(c, k) = draw D + col_off + c + rows_glob k, pairs shared; the
+        // MUFU-based fp32 Box-Muller (common.cuh gauss_pair_f32_fast, ~1e-6 relative per draw), as
+        // the other fp32 sketches
         const int gtid = tid - kF32Cons * 32;
         constexpr int kMaxSl = 4;  // slots per generator thread on the fast path
         const bool even = ((a.rows_glob | (int64_t)a.D | a.col_off) & 1) == 0 && (CT & 1) == 0 &&
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__((kF32Cons + GEN + 1) * 32, 1)
                 for (int i = 0; i < kMaxSl; ++i) {
                     if (i < ns) {
                         float z0, z1;
-                        gauss_pair_f32_state(st[i], z0, z1);
+                        gauss_pair_f32_fast(st[i], z0, z1);
                         const int c = 2 * jjs[i];
                         O[c * a.Kp + ks[i]] = c < ncol ? z0 : 0.f;
                         O[(c + 1) * a.Kp + ks[i]] = c + 1 < ncol ? z1 : 0.f;
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__((kF32Cons + GEN + 1) * 32, 1)
                 const uint64_t p = (s0 >> 1) + (uint64_t)jj;
                 if (p > ((s0 + (uint64_t)CT - 1ull) >> 1)) continue;
                 float z0, z1;
-                gauss_pair(a.seed, p, z0, z1);
+                gauss_pair_f32_fast(a.seed + (2ull * p + 1ull) * 0x9E3779B97F4A7C15ull, z0, z1);
                 const int64_t cc = (int64_t)(2ull * p - s0);
                 if (cc >= 0 && cc < CT) O[cc * a.Kp + k] = cc < ncol ? z0 : 0.f;
                 if (cc + 1 >= 0 && cc + 1 < CT) O[(cc + 1) * a.Kp + k] = cc + 1 < ncol ? z1 : 0.f;
