@@ -103,6 +103,12 @@ size_t tc_ttm_f32_scratch(int64_t dim, int64_t K);  // bytes of the split Q oper
 void launch_tc_ttm_f32(const TTMPlan& p, const void* in, void* out, bool f64_out, const double* q, int64_t ldq,
                        float* scratch, int num_sms, cudaStream_t s);
 
+// ---- fp32 sketch for modes with left % 32 == 0 and K >= 32 on tcgen05 (tc_f32.cu): partial = parts x dim x K
+bool tc_sketch_n_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t right);
+int tc_sketch_n_f32_parts(int64_t left, int64_t dim, int K, int64_t right, int num_sms);
+int launch_tc_sketch_n_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
+                           cudaStream_t s);
+
 // ---- fp32 register-tiled FFMA kernels for modes with left > 1 (slab_f32.cu); fp32 in and out
 bool slab_f32_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right);
 void launch_slab_f32_ttm(const TTMPlan& p, const void* in, void* out, const double* m, int num_sms, cudaStream_t s);

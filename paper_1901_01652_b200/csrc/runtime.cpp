@@ -509,6 +509,13 @@ void sketch_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, co
             gc = trg::launch_stream_sketch_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
         }, yout ? 2 : 1);
         if (defer) *yp = YParts{partial, gc};
+    } else if (p.left > 1 && trg::tc_sketch_n_f32_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
+        const int gc = trg::tc_sketch_n_f32_parts(p.left, p.dim, (int)Kn, p.right, ctx->num_sms);
+        partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);
+        ctx->launch("sketch_m" + std::to_string(n), [&] {
+            trg::launch_tc_sketch_n_f32(p, cur, partial, yout, ctx->num_sms, ctx->stream);
+        }, yout ? 2 : 1);
+        if (defer) *yp = YParts{partial, gc};
     } else if (trg::st_sketch_ok(p.dtype, p.left, p.dim, (int)Kn, p.right)) {
         const int gc = trg::st_sketch_grid(p.left, p.dim, (int)Kn, p.right, ctx->num_sms);
         partial = (double*)ctx->tmp(sizeof(double) * gc * p.dim * Kn);

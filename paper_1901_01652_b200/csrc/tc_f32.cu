@@ -680,6 +680,206 @@ __global__ void __launch_bounds__(kTtThreads, 1)
     }
 }
 
+// ================================================================== K1 for modes n >= 1 (left > 1)
+// Y_n (dim x K) += sum_r P_r Omega_r, P_r = the (dim x left) slab r of P^(n) (left contiguous: the
+// K-major A operand of k_tc_ttm_f32, landed by the same 2-D TMA over [dim right][left] in
+// 128B-swizzled 32-column boxes), Omega_r = its rows l + left r of the reference test matrix
+// (sketch.hpp:32-38, 80-83), regenerated on chip by generator warps as the K-major B operand
+// [Omega_hi | Omega_lo] in the TMA 128B-swizzle layout. CTA = (256-row d tile, a contiguous range of
+// the (r, 32-column chunk) items); D = [A Omega_hi | A Omega_lo] + A_lo Omega_hi in TMEM for the
+// whole range (a few hundred accumulation steps: ~1e-6 relative), drained once into the CTA's fp64
+// partial (partial[range] covers every d tile of that range: the fixed-order split-K reduce sums
+// ranges). Warps: 0 TMA, 1 MMA (+ TMEM), 2-5 splitters, 6-9 generators, then the drain.
+constexpr int kSnThreads = 10 * 32;
+constexpr int kSnGenW0 = 6, kSnGenWarps = 4;
+
+struct TcSnArgs {
+    int left, dim, K, Kp, nchunk, XR, BR, ntd;  // ntd: 256-row d tiles
+    int64_t right, nitems, nparts;
+    uint64_t seed, D;
+    int64_t rows_glob, col_off;
+    double* partial;  // nparts x dim x K
+    uint32_t a_bytes, b_bytes;
+};
+
+__global__ void __launch_bounds__(kSnThreads, 1)
+    k_tc_sketch_n_f32(const __grid_constant__ CUtensorMap pmap, TcSnArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
+    const uint32_t lbase = base + (uint32_t)a.XR * a.a_bytes;
+    const uint32_t bbase = lbase + (uint32_t)kWR * a.a_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (size_t)(a.XR + kWR) * a.a_bytes + (size_t)a.BR * a.b_bytes);
+    uint64_t* xfull = bars;
+    uint64_t* xempty = bars + a.XR;
+    uint64_t* lfull = xempty + a.XR;  // [kWR]
+    uint64_t* lempty = lfull + kWR;   // [kWR]
+    uint64_t* bfull = lempty + kWR;   // [BR]
+    uint64_t* bempty = bfull + a.BR;  // [BR]
+    uint64_t* dfull = bempty + a.BR;  // [1]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dfull + 1);
+    auto X = [&](int r) { return base + (uint32_t)r * a.a_bytes; };
+    auto LO = [&](int w) { return lbase + (uint32_t)w * a.a_bytes; };
+    auto B = [&](int b) { return bbase + (uint32_t)b * a.b_bytes; };
+    const uint32_t tw = 2u * (uint32_t)a.Kp;  // accumulator width per 128-row half
+    const uint32_t tcols = 2 * tw <= 32 ? 32u : 2 * tw <= 64 ? 64u : 2 * tw <= 128 ? 128u : 256u;
+    const int dt = (int)(blockIdx.x % a.ntd), part = (int)(blockIdx.x / a.ntd);
+    const int64_t it0 = a.nitems * part / a.nparts, it1 = a.nitems * (part + 1) / a.nparts;
+    const int total = (int)(it1 - it0);
+    const int d0 = 256 * dt;
+
+    // B ring: rows K..Kp-1 (and Kp+K..2Kp-1) stay zero
+    for (uint32_t o = threadIdx.x * 16u; o < (uint32_t)a.BR * a.b_bytes; o += kSnThreads * 16u)
+        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(bbase + o), "r"(0u));
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < a.XR; ++r) {
+            mbar_init(&xfull[r], 1);
+            mbar_init(&xempty[r], 1);
+        }
+        for (int w = 0; w < kWR; ++w) {
+            mbar_init(&lfull[w], kSplitWarps);
+            mbar_init(&lempty[w], 1);
+        }
+        for (int b = 0; b < a.BR; ++b) {
+            mbar_init(&bfull[b], kSnGenWarps);
+            mbar_init(&bempty[b], 1);
+        }
+        mbar_init(dfull, 1);
+        fence_mbar_init();
+    }
+    fence_async_smem();
+    if (warp == 1) tmem_alloc(tmem_slot, tcols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = policy_l2(0);
+            griddep_wait();
+            for (int g = 0; g < total; ++g) {
+                const int64_t it = it0 + g;
+                const int64_t r = it / a.nchunk;
+                const int ch = (int)(it - r * a.nchunk);
+                const int row = (int)(d0 + (int64_t)a.dim * r);
+                const int x = g % a.XR;
+                if (g >= a.XR) mbar_wait(&xempty[x], ((g / a.XR) - 1) & 1);
+                mbar_arrive_expect_tx(&xfull[x], a.a_bytes);
+                tma2d(X(x), &pmap, 32 * ch, row, &xfull[x], pol);
+                tma2d(X(x) + a.a_bytes / 2, &pmap, 32 * ch, row + 128, &xfull[x], pol);
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc1 = idesc_tf32(128, 2 * a.Kp, 0, 0);
+        const uint32_t idesc2 = idesc_tf32(128, a.Kp, 0, 0);
+        for (int g = 0; g < total; ++g) {
+            const int x = g % a.XR, w = g % kWR, b = g % a.BR;
+            mbar_wait(&xfull[x], (g / a.XR) & 1);
+            mbar_wait(&lfull[w], (g / kWR) & 1);
+            mbar_wait(&bfull[b], (g / a.BR) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {  // 4 k-steps of 8 in the 128-byte rows
+                    const uint64_t bd = sdesc(B(b) + ks * 32u, 16, 1024, kSw128);  // [Omega_hi; Omega_lo] rows
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t ao = (uint32_t)h * (a.a_bytes / 2) + ks * 32u;
+                        const uint64_t xh = sdesc(X(x) + ao, 16, 1024, kSw128);
+                        const uint64_t xl = sdesc(LO(w) + ao, 16, 1024, kSw128);
+                        const uint32_t d = tmem + (uint32_t)h * tw;
+                        const uint32_t acc = (g > 0 || ks > 0) ? 1u : 0u;
+                        mma_tf32(d, xh, bd, idesc1, acc);  // P_hi [Omega_hi | Omega_lo]
+                        mma_tf32(d, xl, bd, idesc2, 1u);   // P_lo Omega_hi (first Kp columns)
+                    }
+                }
+                mma_commit(&xempty[x]);
+                mma_commit(&lempty[w]);
+                mma_commit(&bempty[b]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) mma_commit(dfull);
+        __syncwarp();
+    } else if (warp >= kSplitW0 && warp < kSplitW0 + kSplitWarps) {
+        const int tid = threadIdx.x - kSplitW0 * 32;
+        for (int g = 0; g < total; ++g) {
+            const int x = g % a.XR, w = g % kWR;
+            if (g >= kWR) mbar_wait(&lempty[w], ((g / kWR) - 1) & 1);
+            mbar_wait(&xfull[x], (g / a.XR) & 1);
+            split_lo(X(x), LO(w), a.a_bytes, tid, kSplitWarps * 32);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&lfull[w]);
+        }
+    }
+    if (warp >= kSnGenW0 && warp < kSnGenW0 + kSnGenWarps) {
+        // ---- generators: item (r, ch) -> rows c = 32 ch + l + left r (l < 32) of Omega for every k:
+        // draw D + col_off + c + rows_glob k (sketch.hpp:32-38), pairs (2p, 2p + 1) of the stream;
+        // element (n, l) at row n (hi: k, lo: Kp + k) in the 128B-swizzle layout
+        const int tid = threadIdx.x - kSnGenW0 * 32;
+        const int np = 17;  // pairs covering 32 consecutive draws at either parity
+        for (int g = 0; g < total; ++g) {
+            const int64_t it = it0 + g;
+            const int64_t r = it / a.nchunk;
+            const int ch = (int)(it - r * a.nchunk);
+            const int b = g % a.BR;
+            if (g >= a.BR) mbar_wait(&bempty[b], ((g / a.BR) - 1) & 1);
+            const uint32_t Bb = B(b);
+            const uint64_t c0 = (uint64_t)(a.col_off + 32 * ch + (int64_t)a.left * r);
+            for (int e = tid; e < a.K * np; e += kSnGenWarps * 32) {
+                const int k = e / np, pi = e - k * np;
+                const uint64_t s0 = a.D + c0 + (uint64_t)a.rows_glob * (uint64_t)k;
+                const uint64_t p = (s0 >> 1) + (uint64_t)pi;
+                const int l0 = (int)(2 * p - s0);  // -1 .. 32
+                if (l0 >= 32) continue;
+                float z[2];
+                gauss_pair_f32_fast(a.seed + (2ull * p + 1ull) * 0x9E3779B97F4A7C15ull, z[0], z[1]);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int l = l0 + u;
+                    if (l < 0 || l >= 32) continue;
+                    const float hi = tf32_trunc(z[u]), lo = z[u] - hi;
+                    const uint32_t chunk = (uint32_t)(l >> 2), wb = (uint32_t)(l & 3) * 4u;
+                    const int nh = k, nl = a.Kp + k;
+                    sts32(Bb + (uint32_t)(nh >> 3) * 1024u + (uint32_t)(nh & 7) * 128u + ((chunk ^ (uint32_t)(nh & 7)) << 4) + wb, hi);
+                    sts32(Bb + (uint32_t)(nl >> 3) * 1024u + (uint32_t)(nl & 7) * 128u + ((chunk ^ (uint32_t)(nl & 7)) << 4) + wb, lo);
+                }
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bfull[b]);
+        }
+        // ---- drain: TMEM lane = row of the d tile; Y(d, k) = column k + column Kp + k, fp64
+        mbar_wait(dfull, 0);
+        tc_fence_after();
+        const int q = warp & 3;
+        double* out = a.partial + (int64_t)part * a.dim * a.K;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int d = d0 + h * 128 + q * 32 + lane;
+            for (int n0 = 0; n0 < a.Kp; n0 += 8) {
+                float v[8], u[8];
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)h * tw + (uint32_t)n0;
+                tmem_ld8(ta, v);
+                tmem_ld8(ta + (uint32_t)a.Kp, u);
+                if (d < a.dim)
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        if (n0 + jj < a.K) out[d + (int64_t)a.dim * (n0 + jj)] = (double)v[jj] + (double)u[jj];
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, tcols);
+    }
+}
+
 // Q (fp64, ldq x K column-major, rows [0, I0)) -> Qt_hi / Qt_lo (fp32, Kp x Ip, i fastest),
 // zero-padded: the K2 B operand, split for 3xTF32 (hi = trunc_tf32 of the fp32 rounding)
 __global__ void k_qt_prep(const double* __restrict__ q, int64_t ldq, int I0, int K, int Ip, int Kp, float* hi,
@@ -872,6 +1072,80 @@ void launch_tc_ttm_f32(const TTMPlan& tp, const void* in, void* out, bool f64_ou
         allow_smem(k_tc_ttm_f32<false>, p.smem);
         pdl_launch(k_tc_ttm_f32<false>, dim3(grid), dim3(kTtThreads), p.smem, s, xm, qhm, qlm, a);
     }
+}
+
+
+// ---- K1 for modes n >= 1 on tcgen05 (k_tc_sketch_n_f32)
+namespace {
+struct TcSnPlan {
+    int Kp, nchunk, XR, BR, ntd;
+    int64_t nparts;
+    uint32_t a_bytes, b_bytes;
+    size_t smem;
+};
+bool plan_tc_sketch_n(int64_t left, int64_t dim, int K, int64_t right, int num_sms, TcSnPlan& p) {
+    if (K < 1 || K > 64 || left < 32 || (left % 32) != 0 || dim < 1 || right < 1) return false;
+    if (dim * right + 256 >= (int64_t(1) << 31)) return false;  // TMA row coordinates
+    p.Kp = (K + 15) & ~15;
+    p.nchunk = (int)(left / 32);
+    p.ntd = (int)((dim + 255) / 256);
+    p.a_bytes = 256u * 128u;
+    p.b_bytes = 2u * (uint32_t)p.Kp * 128u;
+    const int64_t nitems = right * p.nchunk;
+    p.nparts = std::max<int64_t>(1, std::min<int64_t>(nitems, num_sms / p.ntd));
+    const size_t fixed = 1024 + 8 * (2 * 8 + 2 * kWR + 2 * 8 + 2) + 64;
+    p.BR = 3;
+    const size_t rest = (size_t)kWR * p.a_bytes + (size_t)p.BR * p.b_bytes + fixed;
+    p.XR = (int)std::min<size_t>(6, (227 * 1024 - rest) / p.a_bytes);
+    p.smem = (size_t)p.XR * p.a_bytes + rest;
+    return p.XR >= 2;
+}
+}  // namespace
+
+bool tc_sketch_n_f32_ok(int dtype, int64_t left, int64_t dim, int K, int64_t right) {
+    TcSnPlan p;
+    if (getenv("TRG_NO_TCGEN05") || (K < 32 && !tc_forced())) return false;
+    return dtype == F32 && encode_fn() && plan_tc_sketch_n(left, dim, K, right, 148, p);
+}
+
+int tc_sketch_n_f32_parts(int64_t left, int64_t dim, int K, int64_t right, int num_sms) {
+    TcSnPlan p;
+    plan_tc_sketch_n(left, dim, K, right, num_sms, p);
+    return (int)p.nparts;
+}
+
+int launch_tc_sketch_n_f32(const SketchPlan& sp, const void* x, double* partial, double* y, int num_sms,
+                           cudaStream_t s) {
+    TcSnPlan p;
+    if (!plan_tc_sketch_n(sp.left, sp.dim, sp.K, sp.right, num_sms, p))
+        throw std::runtime_error("tc sketch (mode >= 1): unsupported shape");
+    TcSnArgs a{};
+    a.left = (int)sp.left;
+    a.dim = (int)sp.dim;
+    a.K = sp.K;
+    a.Kp = p.Kp;
+    a.nchunk = p.nchunk;
+    a.XR = p.XR;
+    a.BR = p.BR;
+    a.ntd = p.ntd;
+    a.right = sp.right;
+    a.nitems = sp.right * p.nchunk;
+    a.nparts = p.nparts;
+    a.seed = sp.seed;
+    a.D = sp.D;
+    a.rows_glob = sp.rows_glob;
+    a.col_off = sp.col_off;
+    a.partial = partial;
+    a.a_bytes = p.a_bytes;
+    a.b_bytes = p.b_bytes;
+    CUtensorMap pm;
+    encode2d(&pm, x, (uint64_t)sp.left, (uint64_t)(sp.dim * sp.right), (uint64_t)sp.left * 4, 32, 128,
+             CU_TENSOR_MAP_SWIZZLE_128B);
+    const int grid = (int)(p.ntd * p.nparts);
+    allow_smem(k_tc_sketch_n_f32, p.smem);
+    pdl_launch(k_tc_sketch_n_f32, dim3(grid), dim3(kSnThreads), p.smem, s, pm, a);
+    if (y) launch_reduce_partials(partial, (int)p.nparts, sp.dim * sp.K, y, s);
+    return (int)p.nparts;
 }
 
 }  // namespace trg

@@ -37,6 +37,11 @@ CASES = [
     ((60, 60, 30), (12, 60, 30)),       # mode 0 only, short fibres (slab_st.cu k_st0_*: C5's mode 0)
     ((400, 50, 21), (20, 50, 21)),      # mode-0 sketch with long fibres, K 20 (C3's mode-0 class)
     ((1000, 7, 9), (20, 7, 9)),         # C3's I_0 = 1000 with few columns (partial fibre stages)
+    # tcgen05 sketch for modes >= 1 (tc_f32.cu k_tc_sketch_n_f32: left % 32 == 0, K >= 32)
+    ((96, 150, 20), (96, 40, 8)),       # left 96 (three 32-column chunks), K 40 (Kp 48)
+    ((64, 300, 7), (64, 48, 3)),        # ragged 256-row d tile (300 = 256 + 44)
+    ((32, 520, 3, 4), (32, 33, 3, 2)),  # three d tiles, K 33 (Kp 48), right 12
+    ((128, 64, 9), (128, 64, 9)),       # mode 1 skipped; left 128 ... then mode 2 left 8192
 ]
 
 
