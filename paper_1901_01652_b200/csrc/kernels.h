@@ -109,6 +109,11 @@ int tc_sketch_n_f32_parts(int64_t left, int64_t dim, int K, int64_t right, int n
 int launch_tc_sketch_n_f32(const SketchPlan& p, const void* x, double* partial, double* y, int num_sms,
                            cudaStream_t s);
 
+bool tc_ttm_n_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right);
+size_t tc_ttm_n_f32_scratch(int64_t dim, int64_t K);  // bytes of the split Q operand
+void launch_tc_ttm_n_f32(const TTMPlan& p, const void* in, void* out, const double* q, int64_t ldq, float* scratch,
+                         int num_sms, cudaStream_t s);
+
 // ---- fp32 register-tiled FFMA kernels for modes with left > 1 (slab_f32.cu); fp32 in and out
 bool slab_f32_ttm_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right);
 void launch_slab_f32_ttm(const TTMPlan& p, const void* in, void* out, const double* m, int num_sms, cudaStream_t s);

@@ -610,6 +610,12 @@ void* shrink_mode(trg_ctx* ctx, const trg_tensor* x, int cdt, const void* cur, c
             trg::launch_tc_ttm_f32(p, cur, out, *odt == F64, m, x->dims[n], scratch, ctx->num_sms, ctx->stream);
         }, 2);
         ctx->tmp_free(scratch);
+    } else if (!promote && p.left > 1 && trg::tc_ttm_n_f32_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
+        float* scratch = (float*)ctx->tmp(trg::tc_ttm_n_f32_scratch(p.dim, Kn));
+        ctx->launch("ttm_m" + std::to_string(n), [&] {
+            trg::launch_tc_ttm_n_f32(p, cur, out, m, x->dims[n], scratch, ctx->num_sms, ctx->stream);
+        }, 2);
+        ctx->tmp_free(scratch);
     } else if (!promote && trg::st0_shrink_ok(p.dtype, p.left, p.dim, Kn, p.right)) {
         ctx->launch("ttm_m" + std::to_string(n), [&] {
             trg::launch_st0_shrink(p, cur, out, m, ctx->num_sms, ctx->stream);

@@ -880,6 +880,178 @@ __global__ void __launch_bounds__(kSnThreads, 1)
     }
 }
 
+// ================================================================== K2 for modes n >= 1 (left > 1)
+// P^(n+1)(l, k, r) = sum_d P(l, d, r) Q(d, k) (tensor.hpp:193-207 with m = Q^T): per output tile
+// (M = 128 rows: 128 consecutive l of one slab r, or 128 / left whole slabs when left is 32 or 64,
+// so the Q chunks stream once per 128 rows) D[M x 2 Kp] = P_r^T [Q_hi | Q_lo] + P_r,lo^T Q_hi over
+// 32-d chunks. A = P_r^T is MN-major (l contiguous): 32-l blocks of 32 d rows by 2-D TMA over
+// [dim right][left] in the 128B-swizzle-of-32-byte-atoms layout (as the mode-0 sketch's X); B = the
+// K-major [Q_hi; Q_lo] chunk (as k_tc_ttm_f32). Double-buffered TMEM accumulators: the epilogue
+// (TMEM lane = l, K values at stride left) overlaps the next tile's MMAs.
+// Warps: 0 TMA, 1 MMA (+ TMEM), 2-5 splitters, 6-9 epilogue.
+struct TcTnArgs {
+    int left, dim, K, Kp, M, nchunk, XR, nlt, S;  // nlt: l tiles per slab; S: slabs per tile (left < 128)
+    int64_t right, ntiles;
+    float* out;
+    uint32_t a_bytes, q_bytes;
+};
+
+__global__ void __launch_bounds__(kTtThreads, 1)
+    k_tc_ttm_n_f32(const __grid_constant__ CUtensorMap pmap, const __grid_constant__ CUtensorMap qhmap,
+                   const __grid_constant__ CUtensorMap qlmap, TcTnArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
+    const uint32_t xbytes = a.a_bytes + 2 * a.q_bytes;  // P^T blocks | Q hi | Q lo
+    const uint32_t lbase = base + (uint32_t)a.XR * xbytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (size_t)a.XR * xbytes + (size_t)kWR * a.a_bytes);
+    uint64_t* xfull = bars;
+    uint64_t* xempty = bars + a.XR;
+    uint64_t* lfull = bars + 2 * a.XR;
+    uint64_t* lempty = lfull + kWR;
+    uint64_t* tfull = lempty + kWR;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    auto X = [&](int r) { return base + (uint32_t)r * xbytes; };
+    auto QH = [&](int r) { return X(r) + a.a_bytes; };
+    auto LO = [&](int w) { return lbase + (uint32_t)w * a.a_bytes; };
+    const uint32_t tw = 2u * (uint32_t)a.Kp;
+    const uint32_t tcols = 2 * tw <= 64 ? 64u : 2 * tw <= 128 ? 128u : 2 * tw <= 256 ? 256u : 512u;
+    const uint32_t lbo_a = 32u * 128u;  // one 32-l block: 32 d rows of 128 B
+    const int nblk = a.M / 32;
+
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < a.XR; ++r) {
+            mbar_init(&xfull[r], 1);
+            mbar_init(&xempty[r], 1);
+        }
+        for (int w = 0; w < kWR; ++w) {
+            mbar_init(&lfull[w], kSplitWarps);
+            mbar_init(&lempty[w], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, tcols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nt = a.ntiles > blockIdx.x ? (int)((a.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const int total = nt * a.nchunk;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_x = policy_l2(0), pol_q = policy_l2(2);
+            griddep_wait();
+            int g = 0;
+            for (int j = 0; j < nt; ++j) {
+                const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
+                const int64_t rt = tile / a.nlt;               // first slab of the tile: rt S
+                const int l0 = (int)(tile - rt * a.nlt) * a.M;  // left >= 128: l offset of the tile
+                const int bps = a.left < 128 ? a.left / 32 : nblk;  // 32-l blocks per slab in the tile
+                for (int ch = 0; ch < a.nchunk; ++ch, ++g) {
+                    const int x = g % a.XR;
+                    if (g >= a.XR) mbar_wait(&xempty[x], ((g / a.XR) - 1) & 1);
+                    mbar_arrive_expect_tx(&xfull[x], (uint32_t)nblk * lbo_a + 2 * a.q_bytes);
+                    for (int b = 0; b < nblk; ++b) {
+                        // block b: 32 l of slab rt S + b / bps (rows past the tensor are zero-filled)
+                        const int64_t r = rt * a.S + b / bps;
+                        const int row = (int)((int64_t)a.dim * r + 32 * ch);
+                        tma2d(X(x) + (uint32_t)b * lbo_a, &pmap, l0 + 32 * (b % bps), row, &xfull[x], pol_x);
+                    }
+                    tma2d(QH(x), &qhmap, 32 * ch, 0, &xfull[x], pol_q);
+                    tma2d(QH(x) + a.q_bytes, &qlmap, 32 * ch, 0, &xfull[x], pol_q);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc1 = idesc_tf32(a.M, 2 * a.Kp, /*a MN-major*/ 1, 0);
+        const uint32_t idesc2 = idesc_tf32(a.M, a.Kp, 1, 0);
+        int g = 0;
+        for (int j = 0; j < nt; ++j) {
+            const int buf = j & 1;
+            if (j >= 2) mbar_wait(&tempty[buf], ((j >> 1) - 1) & 1);
+            tc_fence_after();
+            for (int ch = 0; ch < a.nchunk; ++ch, ++g) {
+                const int x = g % a.XR, w = g % kWR;
+                mbar_wait(&xfull[x], (g / a.XR) & 1);
+                mbar_wait(&lfull[w], (g / kWR) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {  // 4 k-steps of 8 d
+                        const uint64_t qd = sdesc(QH(x) + ks * 32u, 16, 1024, kSw128);
+                        const uint64_t ah = sdesc(X(x) + ks * 1024u, lbo_a, 512, kSw128b32);
+                        const uint64_t al = sdesc(LO(w) + ks * 1024u, lbo_a, 512, kSw128b32);
+                        const uint32_t d = tmem + (uint32_t)buf * tw;
+                        const uint32_t acc = (ch > 0 || ks > 0) ? 1u : 0u;
+                        mma_tf32(d, ah, qd, idesc1, acc);  // P_hi^T [Q_hi | Q_lo]
+                        mma_tf32(d, al, qd, idesc2, 1u);   // P_lo^T Q_hi (first Kp columns)
+                    }
+                    mma_commit(&xempty[x]);
+                    mma_commit(&lempty[w]);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mma_commit(&tfull[buf]);
+            __syncwarp();
+        }
+    } else if (warp >= kSplitW0 && warp < kSplitW0 + kSplitWarps) {
+        const int tid = threadIdx.x - kSplitW0 * 32;
+        const uint32_t real = (uint32_t)nblk * lbo_a;
+        for (int g = 0; g < total; ++g) {
+            const int x = g % a.XR, w = g % kWR;
+            if (g >= kWR) mbar_wait(&lempty[w], ((g / kWR) - 1) & 1);
+            mbar_wait(&xfull[x], (g / a.XR) & 1);
+            split_lo(X(x), LO(w), real, tid, kSplitWarps * 32);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&lfull[w]);
+        }
+    } else {
+        // ================= epilogue: TMEM lane = l of the tile; out(l, k, r) = column k + column Kp + k
+        const int q = warp & 3;
+        for (int j = 0; j < nt; ++j) {
+            const int buf = j & 1;
+            mbar_wait(&tfull[buf], (j >> 1) & 1);
+            tc_fence_after();
+            const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
+            const int64_t rt = tile / a.nlt;
+            // M = 128: lane quarter q holds rows 32 q + lane; M = 64: rows 16 q + lane (lanes 0-15)
+            const int rq = a.M == 128 ? 32 : 16;
+            const int m = q * rq + lane;  // row of the tile: (slab rt S + m / left, l = m % left) when left < 128
+            const int64_t r = a.left < 128 ? rt * a.S + m / a.left : rt;
+            const int l = a.left < 128 ? m % a.left : (int)(tile - rt * a.nlt) * a.M + m;
+            if (r < a.right) {
+                float* o = a.out + l + (int64_t)a.left * a.K * r;
+                for (int n0 = 0; n0 < a.Kp; n0 += 8) {
+                    float v[8], u[8];
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)buf * tw + (uint32_t)n0;
+                    tmem_ld8(ta, v);
+                    tmem_ld8(ta + (uint32_t)a.Kp, u);
+                    if (lane < rq && l < a.left)
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (n0 + jj < a.K) o[(int64_t)a.left * (n0 + jj)] = v[jj] + u[jj];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, tcols);
+    }
+}
+
 // Q (fp64, ldq x K column-major, rows [0, I0)) -> Qt_hi / Qt_lo (fp32, Kp x Ip, i fastest),
 // zero-padded: the K2 B operand, split for 3xTF32 (hi = trunc_tf32 of the fp32 rounding)
 __global__ void k_qt_prep(const double* __restrict__ q, int64_t ldq, int I0, int K, int Ip, int Kp, float* hi,
@@ -1146,6 +1318,84 @@ int launch_tc_sketch_n_f32(const SketchPlan& sp, const void* x, double* partial,
     pdl_launch(k_tc_sketch_n_f32, dim3(grid), dim3(kSnThreads), p.smem, s, pm, a);
     if (y) launch_reduce_partials(partial, (int)p.nparts, sp.dim * sp.K, y, s);
     return (int)p.nparts;
+}
+
+
+// ---- K2 for modes n >= 1 on tcgen05 (k_tc_ttm_n_f32)
+namespace {
+struct TcTnPlan {
+    int Kp, nchunk, XR, Ip, M, nlt, S;
+    uint32_t a_bytes, q_bytes;
+    size_t smem;
+};
+bool plan_tc_ttm_n(int64_t left, int64_t dim, int64_t K, int64_t right, TcTnPlan& p) {
+    if (K < 1 || K > 64 || left < 32 || (left % 32) != 0 || dim < 1 || dim > 4096 || right < 1) return false;
+    if (dim * right + 64 >= (int64_t(1) << 31) || left >= (int64_t(1) << 31)) return false;
+    p.Kp = (int)((K + 15) & ~15);
+    // M = 128 rows per tile: 128 l of one slab, or 128 / left whole slabs when left is 32 or 64
+    if (left < 128 ? (128 % left) != 0 : (left % 128) != 0) return false;
+    p.M = 128;
+    p.S = left < 128 ? (int)(128 / left) : 1;
+    p.nlt = left < 128 ? 1 : (int)(left / 128);
+    p.nchunk = (int)((dim + 31) / 32);
+    p.Ip = p.nchunk * 32;
+    p.a_bytes = (uint32_t)(p.M / 32) * 32u * 128u;
+    p.q_bytes = (uint32_t)p.Kp * 128u;
+    const size_t fixed = 1024 + 8 * (2 * 8 + 2 * kWR + 4) + 64;
+    const size_t lo = (size_t)kWR * p.a_bytes;
+    p.XR = (int)std::min<size_t>(8, (227 * 1024 - fixed - lo) / (p.a_bytes + 2 * (size_t)p.q_bytes));
+    p.smem = (size_t)p.XR * (p.a_bytes + 2 * (size_t)p.q_bytes) + lo + fixed;
+    return p.XR >= 2;
+}
+}  // namespace
+
+bool tc_ttm_n_f32_ok(int dtype, int64_t left, int64_t dim, int64_t K, int64_t right) {
+    TcTnPlan p;
+    if (getenv("TRG_NO_TCGEN05") || (K < 32 && !tc_forced())) return false;
+    return dtype == F32 && encode_fn() && plan_tc_ttm_n(left, dim, K, right, p);
+}
+
+size_t tc_ttm_n_f32_scratch(int64_t dim, int64_t K) {
+    const int Kp = (int)((K + 15) & ~15), Ip = (int)((dim + 31) / 32 * 32);
+    return sizeof(float) * 2 * (size_t)Kp * Ip;
+}
+
+void launch_tc_ttm_n_f32(const TTMPlan& tp, const void* in, void* out, const double* q, int64_t ldq, float* scratch,
+                         int num_sms, cudaStream_t s) {
+    TcTnPlan p;
+    if (!plan_tc_ttm_n(tp.left, tp.dim, tp.odim, tp.right, p)) throw std::runtime_error("tc shrink (mode >= 1): unsupported shape");
+    float* qh = scratch;
+    float* ql = scratch + (size_t)p.Kp * p.Ip;
+    {
+        const int n = p.Kp * p.Ip;
+        pdl_launch(k_qt_prep, dim3(std::min(64, (n + 255) / 256)), dim3(256), 0, s, q, ldq, (int)tp.dim,
+                   (int)tp.odim, p.Ip, p.Kp, qh, ql);
+    }
+    TcTnArgs a{};
+    a.left = (int)tp.left;
+    a.dim = (int)tp.dim;
+    a.K = (int)tp.odim;
+    a.Kp = p.Kp;
+    a.M = p.M;
+    a.nchunk = p.nchunk;
+    a.XR = p.XR;
+    a.nlt = p.nlt;
+    a.S = p.S;
+    a.right = tp.right;
+    a.ntiles = (tp.right + p.S - 1) / p.S * p.nlt;
+    a.out = reinterpret_cast<float*>(out);
+    a.a_bytes = p.a_bytes;
+    a.q_bytes = p.q_bytes;
+    CUtensorMap pm, qhm, qlm;
+    encode2d(&pm, in, (uint64_t)tp.left, (uint64_t)(tp.dim * tp.right), (uint64_t)tp.left * 4, 32, 32,
+             CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    encode2d(&qhm, qh, (uint64_t)p.Ip, (uint64_t)p.Kp, (uint64_t)p.Ip * 4, 32, (uint32_t)p.Kp,
+             CU_TENSOR_MAP_SWIZZLE_128B);
+    encode2d(&qlm, ql, (uint64_t)p.Ip, (uint64_t)p.Kp, (uint64_t)p.Ip * 4, 32, (uint32_t)p.Kp,
+             CU_TENSOR_MAP_SWIZZLE_128B);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, num_sms));
+    allow_smem(k_tc_ttm_n_f32, p.smem);
+    pdl_launch(k_tc_ttm_n_f32, dim3(grid), dim3(kTtThreads), p.smem, s, pm, qhm, qlm, a);
 }
 
 }  // namespace trg
