@@ -694,7 +694,7 @@ constexpr int kSnThreads = 10 * 32;
 constexpr int kSnGenW0 = 6, kSnGenWarps = 4;
 
 struct TcSnArgs {
-    int left, dim, K, Kp, nchunk, XR, BR, ntd;  // ntd: 256-row d tiles
+    int left, dim, K, Kp, nchunk, XR, BR, ntd, TR;  // ntd: d tiles of TR rows (256: two M = 128 halves; 64: one M = 64)
     int64_t right, nitems, nparts;
     uint64_t seed, D;
     int64_t rows_glob, col_off;
@@ -722,12 +722,13 @@ __global__ void __launch_bounds__(kSnThreads, 1)
     auto X = [&](int r) { return base + (uint32_t)r * a.a_bytes; };
     auto LO = [&](int w) { return lbase + (uint32_t)w * a.a_bytes; };
     auto B = [&](int b) { return bbase + (uint32_t)b * a.b_bytes; };
-    const uint32_t tw = 2u * (uint32_t)a.Kp;  // accumulator width per 128-row half
-    const uint32_t tcols = 2 * tw <= 32 ? 32u : 2 * tw <= 64 ? 64u : 2 * tw <= 128 ? 128u : 256u;
+    const uint32_t tw = 2u * (uint32_t)a.Kp;  // accumulator width per M tile
+    const int nh = a.TR == 256 ? 2 : 1;        // M tiles per d tile
+    const uint32_t tcols = nh * tw <= 32 ? 32u : nh * tw <= 64 ? 64u : nh * tw <= 128 ? 128u : 256u;
     const int dt = (int)(blockIdx.x % a.ntd), part = (int)(blockIdx.x / a.ntd);
     const int64_t it0 = a.nitems * part / a.nparts, it1 = a.nitems * (part + 1) / a.nparts;
     const int total = (int)(it1 - it0);
-    const int d0 = 256 * dt;
+    const int d0 = a.TR * dt;
 
     // B ring: rows K..Kp-1 (and Kp+K..2Kp-1) stay zero
     for (uint32_t o = threadIdx.x * 16u; o < (uint32_t)a.BR * a.b_bytes; o += kSnThreads * 16u)
@@ -768,12 +769,13 @@ __global__ void __launch_bounds__(kSnThreads, 1)
                 if (g >= a.XR) mbar_wait(&xempty[x], ((g / a.XR) - 1) & 1);
                 mbar_arrive_expect_tx(&xfull[x], a.a_bytes);
                 tma2d(X(x), &pmap, 32 * ch, row, &xfull[x], pol);
-                tma2d(X(x) + a.a_bytes / 2, &pmap, 32 * ch, row + 128, &xfull[x], pol);
+                if (nh == 2) tma2d(X(x) + a.a_bytes / 2, &pmap, 32 * ch, row + 128, &xfull[x], pol);
             }
         }
     } else if (warp == 1) {
-        const uint32_t idesc1 = idesc_tf32(128, 2 * a.Kp, 0, 0);
-        const uint32_t idesc2 = idesc_tf32(128, a.Kp, 0, 0);
+        const int Mm = nh == 2 ? 128 : 64;
+        const uint32_t idesc1 = idesc_tf32(Mm, 2 * a.Kp, 0, 0);
+        const uint32_t idesc2 = idesc_tf32(Mm, a.Kp, 0, 0);
         for (int g = 0; g < total; ++g) {
             const int x = g % a.XR, w = g % kWR, b = g % a.BR;
             mbar_wait(&xfull[x], (g / a.XR) & 1);
@@ -784,8 +786,7 @@ __global__ void __launch_bounds__(kSnThreads, 1)
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {  // 4 k-steps of 8 in the 128-byte rows
                     const uint64_t bd = sdesc(B(b) + ks * 32u, 16, 1024, kSw128);  // [Omega_hi; Omega_lo] rows
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < nh; ++h) {
                         const uint32_t ao = (uint32_t)h * (a.a_bytes / 2) + ks * 32u;
                         const uint64_t xh = sdesc(X(x) + ao, 16, 1024, kSw128);
                         const uint64_t xl = sdesc(LO(w) + ao, 16, 1024, kSw128);
@@ -852,14 +853,16 @@ __global__ void __launch_bounds__(kSnThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bfull[b]);
         }
-        // ---- drain: TMEM lane = row of the d tile; Y(d, k) = column k + column Kp + k, fp64
+        // ---- drain: TMEM lane = row of the d tile (M = 128: rows 32 q + lane of each half; M = 64:
+        // rows 16 q + lane, lanes 0-15); Y(d, k) = column k + column Kp + k, fp64
         mbar_wait(dfull, 0);
         tc_fence_after();
         const int q = warp & 3;
         double* out = a.partial + (int64_t)part * a.dim * a.K;
+        const int rq = nh == 2 ? 32 : 16;
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            const int d = d0 + h * 128 + q * 32 + lane;
+        for (int h = 0; h < nh; ++h) {
+            const int d = lane < rq ? d0 + h * 128 + q * rq + lane : a.dim;
             for (int n0 = 0; n0 < a.Kp; n0 += 8) {
                 float v[8], u[8];
                 const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)h * tw + (uint32_t)n0;
@@ -1250,7 +1253,7 @@ void launch_tc_ttm_f32(const TTMPlan& tp, const void* in, void* out, bool f64_ou
 // ---- K1 for modes n >= 1 on tcgen05 (k_tc_sketch_n_f32)
 namespace {
 struct TcSnPlan {
-    int Kp, nchunk, XR, BR, ntd;
+    int Kp, nchunk, XR, BR, ntd, TR;
     int64_t nparts;
     uint32_t a_bytes, b_bytes;
     size_t smem;
@@ -1260,8 +1263,9 @@ bool plan_tc_sketch_n(int64_t left, int64_t dim, int K, int64_t right, int num_s
     if (dim * right + 256 >= (int64_t(1) << 31)) return false;  // TMA row coordinates
     p.Kp = (K + 15) & ~15;
     p.nchunk = (int)(left / 32);
-    p.ntd = (int)((dim + 255) / 256);
-    p.a_bytes = 256u * 128u;
+    p.TR = dim <= 64 ? 64 : 256;  // short modes (C5: 60) take one M = 64 tile: no rows of other slabs
+    p.ntd = (int)((dim + p.TR - 1) / p.TR);
+    p.a_bytes = (uint32_t)p.TR * 128u;
     p.b_bytes = 2u * (uint32_t)p.Kp * 128u;
     const int64_t nitems = right * p.nchunk;
     p.nparts = std::max<int64_t>(1, std::min<int64_t>(nitems, num_sms / p.ntd));
@@ -1300,6 +1304,7 @@ int launch_tc_sketch_n_f32(const SketchPlan& sp, const void* x, double* partial,
     a.XR = p.XR;
     a.BR = p.BR;
     a.ntd = p.ntd;
+    a.TR = p.TR;
     a.right = sp.right;
     a.nitems = sp.right * p.nchunk;
     a.nparts = p.nparts;
@@ -1311,8 +1316,8 @@ int launch_tc_sketch_n_f32(const SketchPlan& sp, const void* x, double* partial,
     a.a_bytes = p.a_bytes;
     a.b_bytes = p.b_bytes;
     CUtensorMap pm;
-    encode2d(&pm, x, (uint64_t)sp.left, (uint64_t)(sp.dim * sp.right), (uint64_t)sp.left * 4, 32, 128,
-             CU_TENSOR_MAP_SWIZZLE_128B);
+    encode2d(&pm, x, (uint64_t)sp.left, (uint64_t)(sp.dim * sp.right), (uint64_t)sp.left * 4, 32,
+             (uint32_t)std::min(p.TR, 128), CU_TENSOR_MAP_SWIZZLE_128B);
     const int grid = (int)(p.ntd * p.nparts);
     allow_smem(k_tc_sketch_n_f32, p.smem);
     pdl_launch(k_tc_sketch_n_f32, dim3(grid), dim3(kSnThreads), p.smem, s, pm, a);

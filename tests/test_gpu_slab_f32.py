@@ -42,6 +42,7 @@ CASES = [
     ((64, 300, 7), (64, 48, 3)),        # ragged 256-row d tile (300 = 256 + 44)
     ((32, 520, 3, 4), (32, 33, 3, 2)),  # three d tiles, K 33 (Kp 48), right 12
     ((128, 64, 9), (128, 64, 9)),       # mode 1 skipped; left 128 ... then mode 2 left 8192
+    ((32, 60, 50), (32, 32, 7)),        # dim 60 <= 64: one M = 64 tile per item
     # tcgen05 shrink for modes >= 1 (tc_f32.cu k_tc_ttm_n_f32: left % 64 == 0, K >= 32)
     ((64, 100, 13), (64, 32, 5)),       # two slabs per tile, odd slab count, dim 100 (partial 32-d chunk), K 32
     ((32, 45, 10), (32, 36, 3)),        # left 32: four slabs per tile, right 10 (a partial last tile)
