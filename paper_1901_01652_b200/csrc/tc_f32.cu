@@ -176,7 +176,7 @@ constexpr int kWR = 2;  // lo-ring depth
 static_assert(kSkDrainW0 + kSkDrainWarps == kSkThreads / 32 && kSkGenW0 + kSkGenWarps == kSkDrainW0, "warp roles");
 
 struct TcSkArgs {
-    int I0, K, Kp, M, Mt, nblk, kb, XR, BR, seg, nset, ncat, RS;  // Mt: M tiles per CTA, RS row splits
+    int I0, K, Kp, M, Mt, nblk, kb, XR, BR, seg, nset, ncat, RS, WR;  // WR: lo-ring depth  // Mt: M tiles per CTA, RS row splits
     int64_t L, ntiles;
     uint64_t seed, D;
     int64_t rows_glob, col_off;
@@ -203,14 +203,14 @@ __global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_co
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
     const uint32_t lbase = base + (uint32_t)a.XR * a.a_bytes;
-    const uint32_t bbase = lbase + (uint32_t)kWR * a.a_bytes;
-    const uint32_t ring_bytes = (uint32_t)(a.XR + kWR) * a.a_bytes + (uint32_t)a.BR * 2u * a.b_bytes;
+    const uint32_t bbase = lbase + (uint32_t)a.WR * a.a_bytes;
+    const uint32_t ring_bytes = (uint32_t)(a.XR + a.WR) * a.a_bytes + (uint32_t)a.BR * 2u * a.b_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + ring_bytes);
     uint64_t* xfull = bars;                  // [XR] TMA landed
     uint64_t* xempty = xfull + a.XR;         // [XR] MMAs done with the X slot
     uint64_t* wsplit = xempty + a.XR;        // [2] lo written
-    uint64_t* wempty = wsplit + kWR;         // [2] MMAs done with the lo slot
-    uint64_t* bfull = wempty + kWR;          // [BR] Omega block written
+    uint64_t* wempty = wsplit + a.WR;         // [2] MMAs done with the lo slot
+    uint64_t* bfull = wempty + a.WR;          // [BR] Omega block written
     uint64_t* bempty = bfull + a.BR;         // [BR] MMAs done with the Omega slot
     uint64_t* dfull = bempty + a.BR;         // [2] accumulator set ready to drain
     uint64_t* dempty = dfull + 2;            // [2] accumulator set drained
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_co
             mbar_init(&xfull[r], 1);
             mbar_init(&xempty[r], 1);
         }
-        for (int w = 0; w < kWR; ++w) {
+        for (int w = 0; w < a.WR; ++w) {
             mbar_init(&wsplit[w], kSplitWarps);
             mbar_init(&wempty[w], 1);
         }
@@ -290,10 +290,10 @@ __global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_co
             tc_fence_after();
             const int j1 = min(nt, (g + 1) * a.seg);
             for (int j = g * a.seg; j < j1; ++j) {
-                const int r = j % a.XR, w = j % kWR, bq = j % a.BR;
+                const int r = j % a.XR, w = j % a.WR, bq = j % a.BR;
                 mbar_wait(&xfull[r], (j / a.XR) & 1);
                 if (lane == 0) TC_STAMP(2, j);
-                mbar_wait(&wsplit[w], (j / kWR) & 1);
+                mbar_wait(&wsplit[w], (j / a.WR) & 1);
                 mbar_wait(&bfull[bq], (j / a.BR) & 1);
                 if (lane == 0) TC_STAMP(3, j);
                 tc_fence_after();
@@ -328,8 +328,8 @@ __global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_co
         const int tid = threadIdx.x - kSplitW0 * 32;
         const uint32_t real = (uint32_t)nbc * lbo_a;
         for (int j = 0; j < nt; ++j) {
-            const int r = j % a.XR, w = j % kWR;
-            if (j >= kWR) mbar_wait(&wempty[w], ((j / kWR) - 1) & 1);
+            const int r = j % a.XR, w = j % a.WR;
+            if (j >= a.WR) mbar_wait(&wempty[w], ((j / a.WR) - 1) & 1);
             mbar_wait(&xfull[r], (j / a.XR) & 1);
             if (tid == 0) TC_STAMP(4, j);
             split_lo(X(r), LO(w), real, tid, kSplitWarps * 32);
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_co
 }
 
 struct TcSkPlan {
-    int Kp, M, Mt, RS, nblk, kb, XR, BR, nset, ncat, seg;
+    int Kp, M, Mt, RS, nblk, kb, XR, BR, nset, ncat, seg, WR;
     uint32_t a_bytes, b_bytes;
     size_t smem;
 };
@@ -488,19 +488,31 @@ bool plan_tc_sketch(int64_t I0, int K, TcSkPlan& p) {
     if (p.Mt * (p.ncat ? 2 : 1) * p.Kp > 512) return false;
     p.nblk = (int)((I0 + 31) / 32);
     const int bpc = p.Mt * (p.M / 32);  // blocks per CTA stage
-    // ~32 KB of X per stage
-    p.kb = 8;
-    while (p.kb < 128 && (size_t)bpc * (p.kb * 2) * 128 <= (size_t)env_int("TRG_TC_SK_STAGE", 32768)) p.kb *= 2;
+    // ~32 KB of X per stage with a two-deep lo ring; when that leaves one k-step per stage (all of a
+    // 1024-row I0 in one CTA: C4), 64 KB stages of two k-steps with a one-deep lo ring instead
+    // (C4 sketch_m0 346 -> 311 us: the per-stage barrier and generator overheads were exposed)
+    auto kb_for = [&](size_t stage) {
+        int kb = 8;
+        while (kb < 128 && (size_t)bpc * (kb * 2) * 128 <= stage) kb *= 2;
+        return kb;
+    };
+    p.kb = kb_for((size_t)env_int("TRG_TC_SK_STAGE", 32768));
+    p.WR = kWR;
+    if (p.kb == 8 && !getenv("TRG_TC_SK_STAGE")) {
+        p.kb = kb_for(65536);
+        p.WR = 1;
+    }
+    p.WR = env_int("TRG_TC_SK_WR", p.WR);
     p.seg = p.nset == 2 ? std::max(1, 256 / p.kb) : (1 << 30);  // drain every ~256 columns
     p.a_bytes = (uint32_t)bpc * (uint32_t)p.kb * 128u;
     p.b_bytes = (uint32_t)p.Kp * (uint32_t)p.kb * 4u;
     const size_t fixed = 1024 + 8 * (2 * 8 + 2 * kWR + 2 * 16 + 4) + 64;
-    const size_t budget = 227 * 1024 - fixed - (size_t)kWR * p.a_bytes;
+    const size_t budget = 227 * 1024 - fixed - (size_t)p.WR * p.a_bytes;
     // X ring first (the HBM stream), then the test-matrix ring up to 8 deep
     p.XR = (int)std::min<size_t>(8, (budget - 2 * 2 * (size_t)p.b_bytes) / p.a_bytes);
     p.BR = (int)std::min<size_t>(8, (budget - (size_t)p.XR * p.a_bytes) / (2 * (size_t)p.b_bytes));
     p.XR = env_int("TRG_TC_SK_XR", p.XR);
-    p.smem = (size_t)(p.XR + kWR) * p.a_bytes + (size_t)p.BR * 2 * p.b_bytes + fixed;
+    p.smem = (size_t)(p.XR + p.WR) * p.a_bytes + (size_t)p.BR * 2 * p.b_bytes + fixed;
     return p.XR >= 2 && p.BR >= 2 && p.smem <= 227 * 1024;
 }
 
@@ -1131,6 +1143,7 @@ int launch_tc_sketch_f32(const SketchPlan& sp, const void* x, double* partial, d
     a.Mt = p.Mt;
     a.nblk = p.nblk;
     a.kb = p.kb;
+    a.WR = p.WR;
     a.XR = p.XR;
     a.seg = p.seg;
     a.nset = p.nset;
