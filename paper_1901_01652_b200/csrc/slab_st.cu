@@ -336,6 +336,8 @@ struct StSkArgs {
     uint64_t seed, D;
     int64_t rows_glob, col_off;
     FastDiv div_npr, div_rb;  // Box-Muller pairs per column run; RB
+    FastDiv div_nlb, div_lb;  // l-blocks per slab; LB
+    FastDiv div_npr_m;        // pairs per merged run (LB == left: RB LB consecutive columns per k)
 };
 
 template <int KG, int D, int NC>
@@ -384,10 +386,29 @@ __global__ void __launch_bounds__(NC + 32, 1) k_st_sketch(const __grid_constant_
     // work (K / dim Gaussians per element, C5: 0.2) spreads over all of them instead of being the
     // critical path of a few generator warps. Block layout [rl][l / 4][kq][l % 4][4] (rows padded).
     auto generate = [&](int64_t it, uint32_t n) {
-        const int64_t rbk = it / a.nlb;
+        const int64_t rbk = (int64_t)a.div_nlb.div((uint32_t)it);  // items < 2^31 (plan_st_sketch)
         const int lb = (int)(it - rbk * a.nlb);
         float* O = om + (size_t)(n % kOR) * a.om_floats;
         const int l0 = lb * a.LB;
+        if (a.LB == a.left) {
+            // whole rows: the RB slabs of the item are RB LB consecutive columns of the unfolding, so
+            // each k is one run of RB LB draws (one Box-Muller pair per two columns, no per-slab runs)
+            const int len = a.RB * a.LB;
+            const int64_t rlim = a.right - rbk * a.RB;  // slabs past the tensor's end are zero
+            gen_runs(tid, NC, KG, len, a.div_npr_m, a.seed,
+                     [&](int k) {
+                         return RunInfo{a.D + (uint64_t)(a.col_off + (int64_t)a.left * rbk * a.RB) +
+                                            (uint64_t)a.rows_glob * (uint64_t)(k0 + k),
+                                        k0 + k < a.K, (k >> 2) * 16 + (k & 3)};
+                     },
+                     [&](int base, int c, float z) {
+                         const int rl = (int)a.div_lb.div((uint32_t)c), l = c - rl * a.LB;
+                         O[base + rl * a.NLQ * a.ompitch + (l >> 2) * a.ompitch + (l & 3) * 4] = rl < rlim ? z : 0.f;
+                     });
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ofull[n % kOR]);
+            return;
+        }
         gen_runs(tid, NC, KG * a.RB, a.LB, a.div_npr, a.seed,
                  [&](int q) {
                      const int k = (int)a.div_rb.div((uint32_t)q), rl = q - k * a.RB;
@@ -534,6 +555,7 @@ bool plan_st_sketch(int64_t left, int64_t dim, int K, int64_t right, int num_sms
     p.om_floats = (uint32_t)(((int64_t)p.RB * p.NLQ * p.ompitch + 31) & ~31);
     p.npmax = p.LB / 2 + 1;
     if ((int64_t)p.KG * p.RB * p.npmax >= (int64_t(1) << 31)) return false;
+    if (p.nitems >= (int64_t(1) << 31)) return false;  // 32-bit item split (FastDiv) in the generator
     const size_t red = 4ull * (size_t)p.RS * p.NLQ * p.DC * p.KG;
     const size_t stage_bytes = 4ull * p.stage_floats, om_bytes = 3ull * 4 * p.om_floats;
     p.stages = (int)std::min<size_t>(kStMaxStages, (200 * 1024 - om_bytes) / stage_bytes);
@@ -783,6 +805,9 @@ int launch_st_sketch(const SketchPlan& sp, const void* x, double* partial, doubl
     a.col_off = sp.col_off;
     a.div_npr = FastDiv((uint32_t)(p.LB / 2 + 1));
     a.div_rb = FastDiv((uint32_t)p.RB);
+    a.div_nlb = FastDiv((uint32_t)p.nlb);
+    a.div_lb = FastDiv((uint32_t)p.LB);
+    a.div_npr_m = FastDiv((uint32_t)(p.RB * p.LB / 2 + 1));
     const dim3 grid(p.gx, p.ngroups, p.nz), block(p.NC + 32);
 #define TRG_STSK(KGV, DV, NCV)                                               \
     do {                                                                     \
