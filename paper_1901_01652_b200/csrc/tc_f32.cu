@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) k_tc_sketch_f32(const __grid_co
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
+                    if (u > 0 && pu[u] >= npair) break;  // past the stage's last pair: no draw
                     const uint64_t d0 = a.D + (uint64_t)(a.col_off + c0) + (uint64_t)a.rows_glob * (uint64_t)ku[u];
                     const uint64_t p = (d0 >> 1) + (uint64_t)pu[u];  // pair p holds draws 2p, 2p + 1
                     gauss_pair_f32_fast(a.seed + (2ull * p + 1ull) * 0x9E3779B97F4A7C15ull, z[u][0], z[u][1]);
