@@ -121,6 +121,16 @@ def kernel_flops(cfg, label):
     return None
 
 
+def fp32_peak():
+    """Measured FFMA ceiling (tools/fp32_peak.cu -> profiles/fp32_peak.json), TFLOP/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp32_peak.json")) as f:
+            d = json.load(f)
+        return max(v for k, v in d.items() if k.endswith("_ffma"))
+    except Exception:
+        return None
+
+
 def fp64_peak():
     try:
         with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
@@ -404,6 +414,14 @@ def main():
             roof["fp64_pipe"] = {"achieved_tflops": tf, "peak_tflops": fp64, "frac": tf / fp64,
                                  "flops_per_launch": fl / world,
                                  "peak_source": "measured (profiles/fp64_peak.json, DMMA m8n8k4 loop)"}
+        fp32 = fp32_peak()
+        if fl and cfg["dtype"] == "f32" and fp32 and dom == "sketch_m0" and cfg["K"][0] < 32:
+            # below K_0 = 32 the fp32 mode-0 sketch runs on the CUDA cores (k_sketch_l1_f32, K_0 FFMA
+            # per element; tc_f32.cu's dispatch rule): its second ceiling is the FFMA pipe
+            tf = fl / world / (kernels[dom]["avg_ms"] * 1e-3) / 1e12
+            roof["fp32_pipe"] = {"achieved_tflops": tf, "peak_tflops": fp32, "frac": tf / fp32,
+                                 "flops_per_launch": fl / world,
+                                 "peak_source": "measured (profiles/fp32_peak.json, FFMA loop)"}
     b_alg, sizes, es = alg_bytes(cfg, args.variant)
     stage = {"alg_bytes": b_alg, "frac": b_alg / world / (ms_step * 1e-3) / 1e9 / peak,
              "definition": "SURVEY §8d B_alg / per-rank step time / measured HBM peak"}
