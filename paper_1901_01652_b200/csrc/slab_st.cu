@@ -531,8 +531,12 @@ bool plan_st_sketch(int64_t left, int64_t dim, int K, int64_t right, int num_sms
     p.D = p.KG <= 16 ? 4 : 3;
     // 16 consumer warps when the accumulators leave the registers for them (KG <= 12: C5), else 8
     p.NC = p.KG <= 12 ? 512 : kStCons;
-    // whole rows of l when short (TMA rows of >= 48 bytes), else 64-wide blocks
-    p.LB = left <= 64 ? (int)left : pick_lb(left, 64);
+    // whole rows of l when short (TMA rows of >= 48 bytes), else 64-wide blocks; when there are too
+    // few slabs for several r-slices per item (right < 4: the last mode of an unprojected tensor,
+    // C5 fused sketch_m4), wider l blocks instead, up to what one d-chunk of consumers holds
+    const int lb_cap = right < 4 ? (int)std::min<int64_t>(256, std::max<int64_t>(64, 4 * (p.NC / ((dim + p.D - 1) / p.D))))
+                                 : 64;
+    p.LB = left <= 64 ? (int)left : pick_lb(left, lb_cap);
     p.NLQ = p.LB / 4;
     if (p.NLQ > p.NC) return false;
     p.NDL = (int)std::min<int64_t>({(dim + p.D - 1) / p.D, (int64_t)p.NC / p.NLQ, (int64_t)256 / p.D});

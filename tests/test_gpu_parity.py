@@ -133,6 +133,24 @@ def test_sketch_fused_variant_parity(trg):
     assert relerr(got.projected, proj) < F64_TOL
 
 
+@pytest.mark.parametrize("dims,K", [
+    ((24, 20, 16, 12), (6, 5, 4, 3)),    # last mode: left 7680, right 1 -> 256-wide l blocks
+    ((20, 16, 12, 9, 2), (5, 4, 3, 3, 2)),  # mode 3: right 2 < 4, left 3840
+    ((60, 12, 10, 8), (12, 3, 3, 2)),    # C5-like first extent, odd slab counts
+])
+def test_sketch_fused_variant_f32(trg, dims, K):
+    """Fused variant on fp32 input: every later-mode sketch reads the original X, so its left
+    extent is the product of the original dims (k_st_sketch, wide l blocks when right < 4)."""
+    x = np.random.default_rng(sum(dims)).standard_normal(dims).astype(np.float32)
+    proj, bases, ys = orc.sketch(x.astype(np.float64), K, 13, variant=1)
+    got = trg.sketch(x, trg.ProjectionSpec(list(K), 13), variant=1)
+    for n in range(len(dims)):
+        if K[n] != dims[n]:
+            assert relerr(got.sketches[n], ys[n]) < F32_TOL
+            assert relerr(got.bases[n], bases[n]) < F32_TOL
+    assert relerr(got.projected, proj) < F32_TOL
+
+
 def test_sketch_householder_fallback_matches(trg):
     # exactly rank-2 unfoldings with K = 5 > rank: Y is rank deficient, CholQR2
     # must hand over to Householder; the captured range is still exact.
