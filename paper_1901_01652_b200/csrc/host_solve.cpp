@@ -557,6 +557,11 @@ Mat ridge_solve(Mat gram, const Mat& rhs) {
 // solvers.hpp:195-205
 Mat ls_solve_qr(const Mat& a, const Mat& b) {
     if (a.r >= a.c) {
+        // the device route first (device_ls.cpp: cuSOLVER Householder QR, the same rank cutoff)
+        Mat x(a.c, b.c);
+        const int st = device_ls_qr(a.a.data(), a.r, a.c, b.a.data(), b.c, x.a.data());
+        if (st == 0) return x;
+        if (st == 1) return ridge_solve(matmul_tn(a, a), matmul_tn(a, b));
         HQR qr(a);
         double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
         for (idx i = 0; i < a.c; ++i) {

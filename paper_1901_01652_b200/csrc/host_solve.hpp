@@ -58,6 +58,10 @@ struct SolveOut {
     double discarded_sq = 0.0;
 };
 
+// Device least squares min ||A x - b|| (A m x n column-major, m >= n; b m x nrhs): 0 solved into x
+// (n x nrhs), 1 rank-deficient by the direct route's cutoff, -1 no device route (device_ls.cpp)
+int device_ls_qr(const double* a, idx m, idx n, const double* b, idx nrhs, double* x);
+
 SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance, idx max_sweeps, std::uint64_t seed);
 SolveOut trsvd(const Tensor& x, double tolerance);
 Tensor reconstruct_full(const Cores& f);
