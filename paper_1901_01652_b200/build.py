@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtrg.so")
 
-SOURCES = ["sketch.cu", "stream_f64.cu", "slab_f64.cu", "slab_tma.cu", "stream_f32.cu", "tc_f32.cu", "slab_f32.cu", "slab_st.cu", "ttm.cu", "qr.cu", "tr.cu", "runtime.cpp", "host_solve.cpp", "device_ls.cpp"]
+SOURCES = ["sketch.cu", "stream_f64.cu", "slab_f64.cu", "slab_tma.cu", "stream_f32.cu", "tc_f32.cu", "slab_f32.cu", "slab_st.cu", "ttm.cu", "qr.cu", "tr.cu", "runtime.cpp", "host_solve.cpp", "device_ls.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -1,0 +1,288 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device least squares for the small solve's direct route (row f2; solvers.hpp:195-205, the
+// ALS update of solvers.hpp:238-251 at C4's 2048-4096 x 400 subchain unfoldings): Householder QR
+// of A on the GPU (cuSOLVER geqrf), the same full-rank test on |R_ii| as the host route, then
+// x = R^-1 (Q^T b) (ormqr + trsm). Householder QR as the reference's ColPivHouseholder-free
+// HouseholderQR: a full-rank system has one solution, so x agrees with the host route up to
+// rounding (the reflector sign convention and blocking differ, not the algorithm).
+//
+// cuSOLVER / cuBLAS are library code here (as cuBLAS GEMMs are for plain GEMMs), loaded with
+// dlopen by soname at first use, so libtrg.so carries no link-time dependency on them and shares
+// the copies a PyTorch process may already have loaded. TRG_HOST_LS=1 keeps every solve on the
+// host (A/B tests); without a CUDA device the host route runs, as before.
+//
+// device_als_direct builds the system on the GPU as well: the subchain of the other cores
+// (tr_factors.hpp:111-119; one cuBLAS DGEMM per chain_contract, tr_factors.hpp:92-102), its
+// mode-1 TR unfolding (tensor.hpp:147-157) and the transposed right-hand side by two permutation
+// kernels, so only the cores (tens of KB) and X_<n> (1-2 MB) cross PCIe per update instead of the
+// 6-13 MB system matrix, and the host's subchain / unfold passes disappear.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <limits>
+#include <mutex>
+#include <vector>
+
+#include "host_solve.hpp"
+
+namespace trg {
+namespace host {
+
+namespace {
+
+struct DevLs {
+    bool ok = false;
+    decltype(&cusolverDnCreate) create = nullptr;
+    decltype(&cusolverDnSetStream) set_stream = nullptr;
+    decltype(&cusolverDnDgeqrf_bufferSize) geqrf_ws = nullptr;
+    decltype(&cusolverDnDgeqrf) geqrf = nullptr;
+    decltype(&cusolverDnDormqr_bufferSize) ormqr_ws = nullptr;
+    decltype(&cusolverDnDormqr) ormqr = nullptr;
+    decltype(&cublasCreate_v2) cb_create = nullptr;
+    decltype(&cublasSetStream_v2) cb_set_stream = nullptr;
+    decltype(&cublasDtrsm_v2) trsm = nullptr;
+    decltype(&cublasDgemm_v2) gemm = nullptr;
+    cusolverDnHandle_t sh = nullptr;
+    cublasHandle_t bh = nullptr;
+    cudaStream_t stream = nullptr;
+    int device = -1;
+    // device buffers, grown on demand: A (m x n), B (m x nrhs), tau, workspace, info
+    double *dA = nullptr, *dB = nullptr, *dtau = nullptr, *dwork = nullptr;
+    // device-built systems: cores, X_<n>, two subchain ping-pong buffers
+    double *dG = nullptr, *dXt = nullptr, *dS0 = nullptr, *dS1 = nullptr;
+    int* dinfo = nullptr;
+    size_t capA = 0, capB = 0, capT = 0, capW = 0, capG = 0, capX = 0, capS0 = 0, capS1 = 0;
+};
+
+template <class F>
+bool sym(void* lib, const char* name, F& f) {
+    f = reinterpret_cast<F>(dlsym(lib, name));
+    return f != nullptr;
+}
+
+DevLs* dev_ls() {
+    static DevLs d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (getenv("TRG_HOST_LS")) return;
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            return;
+        }
+        void* ls = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+        void* lb = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+        if (!ls || !lb) return;
+        if (!(sym(ls, "cusolverDnCreate", d.create) && sym(ls, "cusolverDnSetStream", d.set_stream) &&
+              sym(ls, "cusolverDnDgeqrf_bufferSize", d.geqrf_ws) && sym(ls, "cusolverDnDgeqrf", d.geqrf) &&
+              sym(ls, "cusolverDnDormqr_bufferSize", d.ormqr_ws) && sym(ls, "cusolverDnDormqr", d.ormqr) &&
+              sym(lb, "cublasCreate_v2", d.cb_create) && sym(lb, "cublasSetStream_v2", d.cb_set_stream) &&
+              sym(lb, "cublasDtrsm_v2", d.trsm) && sym(lb, "cublasDgemm_v2", d.gemm)))
+            return;
+        if (cudaGetDevice(&d.device) != cudaSuccess) return;
+        if (cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess) return;
+        if (d.create(&d.sh) != CUSOLVER_STATUS_SUCCESS || d.set_stream(d.sh, d.stream) != CUSOLVER_STATUS_SUCCESS)
+            return;
+        if (d.cb_create(&d.bh) != CUBLAS_STATUS_SUCCESS || d.cb_set_stream(d.bh, d.stream) != CUBLAS_STATUS_SUCCESS)
+            return;
+        if (cudaMalloc(&d.dinfo, sizeof(int)) != cudaSuccess) return;
+        d.ok = true;
+    });
+    return d.ok ? &d : nullptr;
+}
+
+bool grow(double*& p, size_t& cap, size_t n) {
+    if (n <= cap) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, n * sizeof(double)) != cudaSuccess) return false;
+    cap = n;
+    return true;
+}
+
+}  // namespace
+
+namespace {
+
+// one set of device buffers, so one solve at a time
+std::mutex g_mu;
+
+// A (m x n, ld m) and B (m x nrhs, ld m) already in d->dA / d->dB on d->stream: Householder QR,
+// the host route's |R_ii| cutoff, x = R^-1 (Q^T B) into x (n x nrhs, host).
+// 0: solved; 1: rank-deficient (caller: ridge); -1: device failure (caller: host route)
+int factor_solve(DevLs* d, idx m, idx n, idx nrhs, double* x, std::chrono::steady_clock::time_point& t0) {
+    const int M = (int)m, Nn = (int)n, R = (int)nrhs;
+    cudaStream_t s = d->stream;
+    const bool prof = solve_prof_on();
+    auto lap = [&](int ph) {
+        if (!prof) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        solve_prof_add(ph, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    };
+    lap(kPhLsH2D);
+    if (d->geqrf(d->sh, M, Nn, d->dA, M, d->dtau, d->dwork, (int)d->capW, d->dinfo) != CUSOLVER_STATUS_SUCCESS)
+        return -1;
+    // |R_ii|: the diagonal of the factored A (stride m + 1)
+    std::vector<double> diag((size_t)n);
+    if (cudaMemcpy2DAsync(diag.data(), sizeof(double), d->dA, sizeof(double) * (m + 1), sizeof(double), (size_t)n,
+                          cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return -1;
+    lap(kPhLsFactor);
+    double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
+    for (double v : diag) {
+        dmax = std::max(dmax, std::abs(v));
+        dmin = std::min(dmin, std::abs(v));
+    }
+    const double cutoff = dmax * static_cast<double>(std::max(m, n)) * std::numeric_limits<double>::epsilon() * 16.0;
+    if (!(dmax > 0.0 && dmin > cutoff)) return 1;
+    if (d->ormqr(d->sh, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, M, R, Nn, d->dA, M, d->dtau, d->dB, M, d->dwork, (int)d->capW,
+                 d->dinfo) != CUSOLVER_STATUS_SUCCESS)
+        return -1;
+    const double one = 1.0;
+    if (d->trsm(d->bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, Nn, R, &one, d->dA,
+                M, d->dB, M) != CUBLAS_STATUS_SUCCESS)
+        return -1;
+    // x = the top n rows of B
+    if (cudaMemcpy2DAsync(x, sizeof(double) * n, d->dB, sizeof(double) * m, sizeof(double) * n, (size_t)nrhs,
+                          cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return -1;
+    lap(kPhLsApply);
+    return 0;
+}
+
+// workspaces for an m x n system with nrhs right-hand sides
+bool reserve(DevLs* d, idx m, idx n, idx nrhs) {
+    if (!grow(d->dA, d->capA, (size_t)m * n) || !grow(d->dB, d->capB, (size_t)m * nrhs) ||
+        !grow(d->dtau, d->capT, (size_t)n))
+        return false;
+    int lw1 = 0, lw2 = 0;
+    if (d->geqrf_ws(d->sh, (int)m, (int)n, d->dA, (int)m, &lw1) != CUSOLVER_STATUS_SUCCESS ||
+        d->ormqr_ws(d->sh, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)m, (int)nrhs, (int)n, d->dA, (int)m, d->dtau, d->dB,
+                    (int)m, &lw2) != CUSOLVER_STATUS_SUCCESS)
+        return false;
+    return grow(d->dwork, d->capW, (size_t)std::max(lw1, lw2));
+}
+
+// small systems stay on the host: below ~1e6 m n^2 the transfers and launches cost more than the
+// factorisation (C1's 100 x 25 systems: 3.5 ms host against 25 ms device per decompose)
+bool device_sized(idx m, idx n, idx nrhs) {
+    return !(m < n || m > (1 << 30) || n < 1 || nrhs < 1 || (double)m * (double)n * (double)n < 1e6);
+}
+
+// unfold_tr(s, 1) of a subchain s (ra, D, rc) (tensor.hpp:147-157 with left = ra, dim = D,
+// right = rc): A(d, r + rc l) = s[l + ra (d + D r)], A column-major D x (rc ra). One thread per
+// output element, consecutive threads on consecutive d: coalesced stores, ra-strided loads
+// (the whole s is L2-resident).
+__global__ void k_unfold_subchain(const double* __restrict__ s, double* __restrict__ a, long long D, int ra, int rc) {
+    const long long total = D * (long long)ra * rc;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long dd = e % D, col = e / D;
+        const int r = (int)(col % rc), l = (int)(col / rc);
+        a[e] = s[l + ra * (dd + D * r)];
+    }
+}
+
+// B = X_<n>^T: xt (rows x cols, column-major) -> b (cols x rows), 32 x 32 tiles through shared memory
+__global__ void k_transpose(const double* __restrict__ xt, double* __restrict__ b, int rows, int cols) {
+    __shared__ double t[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = r0 + threadIdx.x, c = c0 + j;
+        if (r < rows && c < cols) t[j][threadIdx.x] = xt[r + (long long)rows * c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int c = c0 + threadIdx.x, r = r0 + j;
+        if (r < rows && c < cols) b[c + (long long)cols * r] = t[threadIdx.x][j];
+    }
+}
+
+}  // namespace
+
+// 0: solved into x (n x nrhs); 1: rank-deficient by the host route's cutoff (caller: ridge);
+// -1: no device route (caller: host QR)
+int device_ls_qr(const double* a, idx m, idx n, const double* b, idx nrhs, double* x) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!device_sized(m, n, nrhs)) return -1;
+    DevLs* d = dev_ls();
+    if (!d || !reserve(d, m, n, nrhs)) return -1;
+    cudaStream_t s = d->stream;
+    auto t0 = std::chrono::steady_clock::now();
+    if (cudaMemcpyAsync(d->dA, a, sizeof(double) * m * n, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d->dB, b, sizeof(double) * m * nrhs, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return -1;
+    return factor_solve(d, m, n, nrhs, x, t0);
+}
+
+int device_als_direct(const Cores& f, idx n, const Mat& xn_tr, Mat& z) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    const idx N = f.order();
+    const idx rows = xn_tr.c;                                      // prod of the other extents
+    const idx cols = f.rank(n) * f.rank((n + 1) % N);              // R_n R_{n+1}
+    const idx nrhs = xn_tr.r;                                      // I_n
+    if (N < 2 || !device_sized(rows, cols, nrhs)) return -1;
+    DevLs* d = dev_ls();
+    if (!d || !reserve(d, rows, cols, nrhs)) return -1;
+    cudaStream_t s = d->stream;
+    auto t0 = std::chrono::steady_clock::now();
+    // cores n+1, ..., n+N-1 back to back
+    std::vector<size_t> off;
+    size_t tot = 0;
+    for (idx k = 1; k < N; ++k) {
+        off.push_back(tot);
+        tot += f.g[(size_t)((n + k) % N)].data.size();
+    }
+    if (!grow(d->dG, d->capG, tot) || !grow(d->dXt, d->capX, (size_t)(rows * nrhs)) ||
+        !grow(d->dS0, d->capS0, (size_t)(rows * cols)) || !grow(d->dS1, d->capS1, (size_t)(rows * cols)))
+        return -1;
+    for (idx k = 1; k < N; ++k) {
+        const Tensor& g = f.g[(size_t)((n + k) % N)];
+        if (cudaMemcpyAsync(d->dG + off[(size_t)(k - 1)], g.data.data(), sizeof(double) * g.data.size(),
+                            cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return -1;
+    }
+    if (cudaMemcpyAsync(d->dXt, xn_tr.a.data(), sizeof(double) * rows * nrhs, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+        return -1;
+    // subchain (tr_factors.hpp:111-119): cur (ra, p, rb) x g (rb, i, rc) -> (ra, p i, rc) is
+    // out(ra p x i rc) = cur(ra p x rb) * g(rb x i rc), all column-major
+    const Tensor& g0 = f.g[(size_t)((n + 1) % N)];
+    const double* cur = d->dG;
+    idx ra = g0.shape[0], p = g0.shape[1], rb = g0.shape[2];
+    double* bufs[2] = {d->dS0, d->dS1};
+    const double one = 1.0, zero = 0.0;
+    for (idx k = 2; k < N; ++k) {
+        const Tensor& g = f.g[(size_t)((n + k) % N)];
+        const idx i = g.shape[1], rc = g.shape[2];
+        double* out = bufs[k % 2];
+        if (d->gemm(d->bh, CUBLAS_OP_N, CUBLAS_OP_N, (int)(ra * p), (int)(i * rc), (int)rb, &one, cur, (int)(ra * p),
+                    d->dG + off[(size_t)(k - 1)], (int)rb, &zero, out, (int)(ra * p)) != CUBLAS_STATUS_SUCCESS)
+            return -1;
+        cur = out;
+        p *= i;
+        rb = rc;
+    }
+    if (p != rows || ra * rb != cols) return -1;
+    k_unfold_subchain<<<148 * 8, 256, 0, s>>>(cur, d->dA, (long long)rows, (int)ra, (int)rb);
+    const dim3 tb(32, 8), tg((unsigned)((rows + 31) / 32), (unsigned)((nrhs + 31) / 32));
+    k_transpose<<<tg, tb, 0, s>>>(d->dXt, d->dB, (int)nrhs, (int)rows);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    z = Mat(cols, nrhs);
+    return factor_solve(d, rows, cols, nrhs, z.a.data(), t0);
+}
+
+}  // namespace host
+}  // namespace trg

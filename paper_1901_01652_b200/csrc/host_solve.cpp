@@ -3,6 +3,9 @@
 #include "host_solve.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -13,6 +16,26 @@
 
 namespace trg {
 namespace host {
+
+namespace {
+double g_phase_ms[kPhCount];
+const char* const kPhaseName[kPhCount] = {"subchain", "unfold", "ls_h2d", "ls_factor", "ls_apply", "ls_host", "store", "rse"};
+struct PhaseTimer {
+    int ph;
+    std::chrono::steady_clock::time_point t0;
+    explicit PhaseTimer(int p) : ph(p), t0(std::chrono::steady_clock::now()) {}
+    ~PhaseTimer() {
+        if (solve_prof_on())
+            solve_prof_add(ph, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+}  // namespace
+
+bool solve_prof_on() {
+    static const bool on = getenv("TRG_SOLVE_PROF") != nullptr;
+    return on;
+}
+void solve_prof_add(int phase, double ms) { g_phase_ms[phase] += ms; }
 
 namespace {
 
@@ -557,11 +580,12 @@ Mat ridge_solve(Mat gram, const Mat& rhs) {
 // solvers.hpp:195-205
 Mat ls_solve_qr(const Mat& a, const Mat& b) {
     if (a.r >= a.c) {
-        // the device route first (device_ls.cpp: cuSOLVER Householder QR, the same rank cutoff)
+        // the device route first (device_ls.cu: cuSOLVER Householder QR, the same rank cutoff)
         Mat x(a.c, b.c);
         const int st = device_ls_qr(a.a.data(), a.r, a.c, b.a.data(), b.c, x.a.data());
         if (st == 0) return x;
         if (st == 1) return ridge_solve(matmul_tn(a, a), matmul_tn(a, b));
+        PhaseTimer t(kPhLsHost);
         HQR qr(a);
         double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
         for (idx i = 0; i < a.c; ++i) {
@@ -671,11 +695,29 @@ void als_update_mode(const Mat& xn_tr, Cores& f, idx n) {
     const idx m = f.rank(n) * f.rank((n + 1) % f.order());
     Mat z;
     if (n_cols <= kDirectLsMaxRows && n_cols >= m) {
-        const Tensor s = subchain(f, n);
-        z = ls_solve_qr(unfold_tr(s, 1), transpose(xn_tr));
+        // the system built and solved on the device when it is large enough (device_ls.cu)
+        const int st = device_als_direct(f, n, xn_tr, z);
+        if (st == 0) {
+            PhaseTimer t(kPhStore);
+            store_core(f.g[static_cast<size_t>(n)], z);
+            return;
+        }
+        Tensor s;
+        {
+            PhaseTimer t(kPhSubchain);
+            s = subchain(f, n);
+        }
+        Mat a, b;
+        {
+            PhaseTimer t(kPhUnfold);
+            a = unfold_tr(s, 1);
+            b = transpose(xn_tr);
+        }
+        z = ls_solve_qr(a, b);
     } else {
         z = ls_solve_gram(subchain_gram(f, n), transpose(subchain_rhs(xn_tr, f, n)));
     }
+    PhaseTimer t(kPhStore);
     store_core(f.g[static_cast<size_t>(n)], z);
 }
 
@@ -894,12 +936,21 @@ SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance,
     SolveOut o;
     for (idx sweep = 1; sweep <= max_sweeps; ++sweep) {
         for (idx n = 0; n < N; ++n) als_update_mode(unf[static_cast<size_t>(n)], f, n);
-        o.rse_history.push_back(rse(x, reconstruct_full(f)));
+        {
+            PhaseTimer t(kPhRse);
+            o.rse_history.push_back(rse(x, reconstruct_full(f)));
+        }
         o.sweeps_run = sweep;
         const size_t k = o.rse_history.size();
         if (k >= 2 && std::abs(o.rse_history[k - 1] - o.rse_history[k - 2]) < tolerance * o.rse_history[k - 2]) break;
     }
     o.cores = std::move(f);
+    if (solve_prof_on()) {
+        for (int p = 0; p < kPhCount; ++p) {
+            fprintf(stderr, "[trg solve] %-10s %9.3f ms\n", kPhaseName[p], g_phase_ms[p]);
+            g_phase_ms[p] = 0.0;
+        }
+    }
     return o;
 }
 

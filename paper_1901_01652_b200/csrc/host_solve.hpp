@@ -59,8 +59,19 @@ struct SolveOut {
 };
 
 // Device least squares min ||A x - b|| (A m x n column-major, m >= n; b m x nrhs): 0 solved into x
-// (n x nrhs), 1 rank-deficient by the direct route's cutoff, -1 no device route (device_ls.cpp)
+// (n x nrhs), 1 rank-deficient by the direct route's cutoff, -1 no device route (device_ls.cu)
 int device_ls_qr(const double* a, idx m, idx n, const double* b, idx nrhs, double* x);
+
+// The direct-route ALS update with the system built on the device (device_ls.cu): subchain of
+// cores n+1..n+N-1, its mode-1 TR unfolding and B = X_<n>^T, then the device_ls_qr solve.
+// 0: z = (R_n R_{n+1}) x I_n solution; 1 rank-deficient; -1 no device route.
+int device_als_direct(const Cores& f, idx n, const Mat& xn_tr, Mat& z);
+
+// Phase timers of the small solve, on only with TRG_SOLVE_PROF=1 (printed to stderr after each
+// trals call; the device phases then synchronise after each step so the split is attributable).
+enum SolvePhase { kPhSubchain, kPhUnfold, kPhLsH2D, kPhLsFactor, kPhLsApply, kPhLsHost, kPhStore, kPhRse, kPhCount };
+bool solve_prof_on();
+void solve_prof_add(int phase, double ms);
 
 SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance, idx max_sweeps, std::uint64_t seed);
 SolveOut trsvd(const Tensor& x, double tolerance);
