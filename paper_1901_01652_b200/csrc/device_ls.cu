@@ -57,8 +57,11 @@ struct DevLs {
     double *dA = nullptr, *dB = nullptr, *dtau = nullptr, *dwork = nullptr;
     // device-built systems: cores, X_<n>, two subchain ping-pong buffers
     double *dG = nullptr, *dXt = nullptr, *dS0 = nullptr, *dS1 = nullptr;
+    // per-sweep RSE: reconstruction, mode-1 unfolding of core 0, block partial sums
+    double *dY = nullptr, *dC = nullptr, *dPart = nullptr;
     int* dinfo = nullptr;
-    size_t capA = 0, capB = 0, capT = 0, capW = 0, capG = 0, capX = 0, capS0 = 0, capS1 = 0;
+    size_t capA = 0, capB = 0, capT = 0, capW = 0, capG = 0, capX = 0, capS0 = 0, capS1 = 0, capY = 0, capC = 0,
+           capPart = 0;
 };
 
 template <class F>
@@ -210,6 +213,85 @@ __global__ void k_transpose(const double* __restrict__ xt, double* __restrict__ 
     }
 }
 
+// reconstruct_full's operands (tr_factors.hpp:123-137 at mode 0): W(a + R0 b, p) =
+// s[b + R1 (p + P a)] for the subchain s = (R1, P, R0) of cores 1..N-1, and core2(i, a + R0 b) =
+// g0[a + R0 (i + I0 b)]; then X_<0> = core2 W is one DGEMM
+__global__ void k_rse_operands(const double* __restrict__ s, const double* __restrict__ g0, double* __restrict__ w,
+                               double* __restrict__ c2, long long P, int R0, int R1, int I0) {
+    const long long nw = P * R0 * R1, nc = (long long)I0 * R0 * R1;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nw + nc;
+         e += (long long)gridDim.x * blockDim.x) {
+        if (e < nw) {
+            const long long q = e % ((long long)R0 * R1), p = e / ((long long)R0 * R1);
+            const int a = (int)(q % R0), b = (int)(q / R0);
+            w[e] = s[b + R1 * (p + P * a)];
+        } else {
+            const long long f = e - nw;
+            const long long i = f % I0, q = f / I0;
+            const int a = (int)(q % R0), b = (int)(q / R0);
+            c2[f] = g0[a + R0 * (i + (long long)I0 * b)];
+        }
+    }
+}
+
+// per-block sums of (x - y)^2 and x^2 (solvers.hpp:47-54); fixed grid and tree: deterministic
+constexpr int kRseBlocks = 148 * 2;
+__global__ void __launch_bounds__(256) k_rse_partials(const double* __restrict__ x, const double* __restrict__ y,
+                                                      long long n, double* __restrict__ part) {
+    double num = 0.0, den = 0.0;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+        const double v = x[e], dd = v - y[e];
+        num = fma(dd, dd, num);
+        den = fma(v, v, den);
+    }
+    __shared__ double sn[8], sd[8];
+    for (int o = 16; o; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sn[threadIdx.x >> 5] = num;
+        sd[threadIdx.x >> 5] = den;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a += sn[w];
+            b += sd[w];
+        }
+        part[2 * blockIdx.x] = a;
+        part[2 * blockIdx.x + 1] = b;
+    }
+}
+
+// subchain of cores first, first+1, ..., first+N-2 (mod N) into one of two ping-pong buffers; the
+// cores are at d->dG + off[k - 1] for chain position k = 1..N-1. Returns the result pointer and
+// its shape (ra, p, rb), or nullptr on a cuBLAS failure.
+const double* device_subchain(DevLs* d, const Cores& f, idx first, const std::vector<size_t>& off, idx& ra, idx& p,
+                              idx& rb) {
+    const idx N = f.order();
+    const Tensor& g0 = f.g[(size_t)(first % N)];
+    const double* cur = d->dG + off[0];
+    ra = g0.shape[0];
+    p = g0.shape[1];
+    rb = g0.shape[2];
+    double* bufs[2] = {d->dS0, d->dS1};
+    const double one = 1.0, zero = 0.0;
+    for (idx k = 2; k < N; ++k) {
+        const Tensor& g = f.g[(size_t)((first + k - 1) % N)];
+        const idx i = g.shape[1], rc = g.shape[2];
+        double* out = bufs[k % 2];
+        if (d->gemm(d->bh, CUBLAS_OP_N, CUBLAS_OP_N, (int)(ra * p), (int)(i * rc), (int)rb, &one, cur, (int)(ra * p),
+                    d->dG + off[(size_t)(k - 1)], (int)rb, &zero, out, (int)(ra * p)) != CUBLAS_STATUS_SUCCESS)
+            return nullptr;
+        cur = out;
+        p *= i;
+        rb = rc;
+    }
+    return cur;
+}
+
 }  // namespace
 
 // 0: solved into x (n x nrhs); 1: rank-deficient by the host route's cutoff (caller: ridge);
@@ -259,22 +341,9 @@ int device_als_direct(const Cores& f, idx n, const Mat& xn_tr, Mat& z) {
         return -1;
     // subchain (tr_factors.hpp:111-119): cur (ra, p, rb) x g (rb, i, rc) -> (ra, p i, rc) is
     // out(ra p x i rc) = cur(ra p x rb) * g(rb x i rc), all column-major
-    const Tensor& g0 = f.g[(size_t)((n + 1) % N)];
-    const double* cur = d->dG;
-    idx ra = g0.shape[0], p = g0.shape[1], rb = g0.shape[2];
-    double* bufs[2] = {d->dS0, d->dS1};
-    const double one = 1.0, zero = 0.0;
-    for (idx k = 2; k < N; ++k) {
-        const Tensor& g = f.g[(size_t)((n + k) % N)];
-        const idx i = g.shape[1], rc = g.shape[2];
-        double* out = bufs[k % 2];
-        if (d->gemm(d->bh, CUBLAS_OP_N, CUBLAS_OP_N, (int)(ra * p), (int)(i * rc), (int)rb, &one, cur, (int)(ra * p),
-                    d->dG + off[(size_t)(k - 1)], (int)rb, &zero, out, (int)(ra * p)) != CUBLAS_STATUS_SUCCESS)
-            return -1;
-        cur = out;
-        p *= i;
-        rb = rc;
-    }
+    idx ra = 0, p = 0, rb = 0;
+    const double* cur = device_subchain(d, f, n + 1, off, ra, p, rb);
+    if (!cur) return -1;
     if (p != rows || ra * rb != cols) return -1;
     k_unfold_subchain<<<148 * 8, 256, 0, s>>>(cur, d->dA, (long long)rows, (int)ra, (int)rb);
     const dim3 tb(32, 8), tg((unsigned)((rows + 31) / 32), (unsigned)((nrhs + 31) / 32));
@@ -282,6 +351,64 @@ int device_als_direct(const Cores& f, idx n, const Mat& xn_tr, Mat& z) {
     if (cudaGetLastError() != cudaSuccess) return -1;
     z = Mat(cols, nrhs);
     return factor_solve(d, rows, cols, nrhs, z.a.data(), t0);
+}
+
+// rse(x, reconstruct_full(f)) on the device (solvers.hpp:47-54, tr_factors.hpp:123-137): the
+// subchain of cores 1..N-1 and X_<0> = core2 W by cuBLAS, the squared sums by k_rse_partials,
+// summed on the host in block order. 0: *out set; -1: no device route (caller: host).
+int device_tr_rse(const Cores& f, const Tensor& x, double* out) {
+    const idx N = f.order();
+    if (N < 2) return -1;
+    const idx R0 = f.rank(0), R1 = f.rank(1 % N), I0 = f.dim(0);
+    const idx P = x.size() / I0;
+    // below ~1e7 multiply-adds the host reconstruction is faster than the round trip
+    if ((double)x.size() * (double)(R0 * R1) < 1e7) return -1;
+    std::lock_guard<std::mutex> lock(g_mu);
+    DevLs* d = dev_ls();
+    if (!d) return -1;
+    std::vector<size_t> off;
+    size_t tot = 0;
+    for (idx k = 0; k < N; ++k) {
+        off.push_back(tot);
+        tot += f.g[(size_t)k].data.size();
+    }
+    const size_t nx = (size_t)x.size(), sub = (size_t)(P * R0 * R1);
+    if (!grow(d->dG, d->capG, tot) || !grow(d->dXt, d->capX, nx) || !grow(d->dS0, d->capS0, sub) ||
+        !grow(d->dS1, d->capS1, sub) || !grow(d->dY, d->capY, nx + sub) ||
+        !grow(d->dC, d->capC, (size_t)(I0 * R0 * R1)) || !grow(d->dPart, d->capPart, 2 * kRseBlocks))
+        return -1;
+    cudaStream_t s = d->stream;
+    for (idx k = 0; k < N; ++k)
+        if (cudaMemcpyAsync(d->dG + off[(size_t)k], f.g[(size_t)k].data.data(),
+                            sizeof(double) * f.g[(size_t)k].data.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return -1;
+    if (cudaMemcpyAsync(d->dXt, x.data.data(), sizeof(double) * nx, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return -1;
+    const std::vector<size_t> off1(off.begin() + 1, off.end());
+    idx ra = 0, p = 0, rb = 0;
+    const double* sc = device_subchain(d, f, 1, off1, ra, p, rb);
+    if (!sc || ra != R1 || rb != R0 || p != P) return -1;
+    double* w = d->dY + nx;  // W (R0 R1 x P) after the reconstruction's slot
+    k_rse_operands<<<148 * 4, 256, 0, s>>>(sc, d->dG + off[0], w, d->dC, (long long)P, (int)R0, (int)R1, (int)I0);
+    const double one = 1.0, zero = 0.0;
+    if (d->gemm(d->bh, CUBLAS_OP_N, CUBLAS_OP_N, (int)I0, (int)P, (int)(R0 * R1), &one, d->dC, (int)I0, w,
+                (int)(R0 * R1), &zero, d->dY, (int)I0) != CUBLAS_STATUS_SUCCESS)
+        return -1;
+    k_rse_partials<<<kRseBlocks, 256, 0, s>>>(d->dXt, d->dY, (long long)nx, d->dPart);
+    std::vector<double> part(2 * kRseBlocks);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(part.data(), d->dPart, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return -1;
+    double num = 0.0, den = 0.0;
+    for (int b = 0; b < kRseBlocks; ++b) {
+        num += part[2 * b];
+        den += part[2 * b + 1];
+    }
+    if (!(den > 0.0)) return -1;
+    *out = std::sqrt(num) / std::sqrt(den);
+    return 0;
 }
 
 }  // namespace host

@@ -938,7 +938,8 @@ SolveOut trals(const Tensor& x, const std::vector<idx>& ranks, double tolerance,
         for (idx n = 0; n < N; ++n) als_update_mode(unf[static_cast<size_t>(n)], f, n);
         {
             PhaseTimer t(kPhRse);
-            o.rse_history.push_back(rse(x, reconstruct_full(f)));
+            double e = 0.0;
+            o.rse_history.push_back(device_tr_rse(f, x, &e) == 0 ? e : rse(x, reconstruct_full(f)));
         }
         o.sweeps_run = sweep;
         const size_t k = o.rse_history.size();

@@ -67,6 +67,9 @@ int device_ls_qr(const double* a, idx m, idx n, const double* b, idx nrhs, doubl
 // 0: z = (R_n R_{n+1}) x I_n solution; 1 rank-deficient; -1 no device route.
 int device_als_direct(const Cores& f, idx n, const Mat& xn_tr, Mat& z);
 
+// rse(x, reconstruct_full(f)) on the device (device_ls.cu). 0: *out set; -1: no device route.
+int device_tr_rse(const Cores& f, const Tensor& x, double* out);
+
 // Phase timers of the small solve, on only with TRG_SOLVE_PROF=1 (printed to stderr after each
 // trals call; the device phases then synchronise after each step so the split is attributable).
 enum SolvePhase { kPhSubchain, kPhUnfold, kPhLsH2D, kPhLsFactor, kPhLsApply, kPhLsHost, kPhStore, kPhRse, kPhCount };

@@ -302,6 +302,19 @@ def test_rtrals_c1_parity(trg):
     assert relerr(recon_g, recon_w) < F64_TOL
 
 
+def test_rtrals_order4_device_systems_parity(trg):
+    """Order-4 rTR-ALS whose direct-route systems (16^3 = 4096 x 256) and per-sweep RSE
+    (16^4 x 256 multiply-adds) are large enough to be built and solved on the device
+    (device_ls.cu: device_als_direct, device_tr_rse), against the oracle's host Algorithm 1."""
+    dims, R = [40, 40, 40, 40], 16
+    x = orc.add_noise(orc.reconstruct_full(orc.random_factors(dims, [R] * 4, 3)), 40.0, 4)
+    want = orc.rtrd("als", x, [16] * 4, ranks=[R] * 4, max_sweeps=4, cfg_seed=0, spec_seed=0)
+    got = trg.rtrals(x, trg.SolverConfig(ranks=[R] * 4, max_sweeps=4, seed=0), trg.ProjectionSpec([16] * 4, 0))
+    assert got.sweeps_run == want.sweeps_run == 4
+    np.testing.assert_allclose(got.rse_history, want.rse_history, rtol=F64_TOL)
+    assert relerr(orc.reconstruct_full(got.factors), orc.reconstruct_full(want.cores)) < F64_TOL
+
+
 def test_rtrsvd_parity_with_sign_normalisation(trg):
     dims = [30, 28, 26, 24]
     x = orc.add_noise(orc.reconstruct_full(orc.random_factors(dims, [3] * 4, 0)), 30.0, 1)
