@@ -258,9 +258,44 @@ def cpu_baseline(cfg, budget_s=20.0, steps=1):
         t, nbytes = run(shape)
         ts.append(t)
     sec = float(np.mean(ts))
-    return {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"oracle sketch() of a {'x'.join(map(str, shape))} {cfg['dtype']} tensor "
-                      f"(same K, fp64 compute), {steps} run(s), {sec:.3f} s each, OpenMP {threads} threads"}
+    out = {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+           "sample": f"oracle sketch() of a {'x'.join(map(str, shape))} {cfg['dtype']} tensor "
+                     f"(same K, fp64 compute), {steps} run(s), {sec:.3f} s each, OpenMP {threads} threads"}
+    # SURVEY §8d's faithful single-thread figure (the reference's Eigen path is single-threaded)
+    _, shape1, run1 = cpu_sample(cfg, budget_s / 4.0, 1)
+    orc.set_threads(1)
+    t1, nb1 = run1(shape1)
+    orc.set_threads(threads)
+    out["single_thread"] = {"value": nb1 / t1 / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+                            "sample": f"oracle sketch() of a {'x'.join(map(str, shape1))} tensor, 1 run, "
+                                      f"{t1:.3f} s, 1 thread"}
+    return out
+
+
+def cpu_algorithm1(cfg, threads, max_elems=2.0e8):
+    """Algorithm 1 end to end on the host restatement (oracle rtrd: sketch, small solve,
+    back-projection, final RSE), the CPU figure beside the GPU arm's decompose_e2e. Full size
+    when X has at most max_elems elements, else the bounded sample of cpu_sample."""
+    orc, shape, _ = cpu_sample(cfg, 20.0, 1)
+    if float(np.prod(cfg["dims"])) <= max_elems:
+        shape = list(cfg["dims"])
+    N = len(shape)
+    # the config's tensor family (random TR factors plus noise at the config's SNR), as the GPU arm's
+    x = orc.reconstruct_full(orc.random_factors(shape, [cfg["rank"]] * N, 0, cfg["scale"]))
+    if cfg.get("snr") is not None:
+        x = orc.add_noise(x, cfg["snr"], 1)
+    if cfg["dtype"] == "f32":
+        x = x.astype(np.float32).astype(np.float64)
+    K = [min(k, d) for k, d in zip(cfg["K"], shape)]
+    orc.set_threads(threads)
+    t0 = time.perf_counter()
+    if cfg["method"] == "als":
+        rep = orc.rtrd("als", x, K, ranks=[cfg["rank"]] * N, tol=cfg["tol"], max_sweeps=cfg["sweeps"])
+    else:
+        rep = orc.rtrd("svd", x, K, tol=cfg["tol"])
+    sec = time.perf_counter() - t0
+    return {"seconds": sec, "cores": threads, "kind": "port", "dims": shape, "final_rse": rep.rse_history[-1],
+            "call": "oracle rtrd (rtrals/rtrsvd restatement, sketch.hpp:154-165), fp64, TR factors + noise"}
 
 
 def reference_arm(args, cfg):
@@ -288,6 +323,7 @@ def reference_arm(args, cfg):
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": f"oracle sketch() of a {'x'.join(map(str, shape))} sample per step"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line["algorithm1"] = cpu_algorithm1(cfg, threads)
     print(json.dumps(line), flush=True)
 
 
