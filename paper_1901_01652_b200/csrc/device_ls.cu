@@ -49,6 +49,11 @@ struct DevLs {
     decltype(&cublasSetStream_v2) cb_set_stream = nullptr;
     decltype(&cublasDtrsm_v2) trsm = nullptr;
     decltype(&cublasDgemm_v2) gemm = nullptr;
+    // optional: Jacobi SVD (device_svd); absent symbols leave the host SVD in place
+    decltype(&cusolverDnCreateGesvdjInfo) svdj_info = nullptr;
+    decltype(&cusolverDnDgesvdj_bufferSize) svdj_ws = nullptr;
+    decltype(&cusolverDnDgesvdj) svdj = nullptr;
+    gesvdjInfo_t svdj_params = nullptr;
     cusolverDnHandle_t sh = nullptr;
     cublasHandle_t bh = nullptr;
     cudaStream_t stream = nullptr;
@@ -89,6 +94,12 @@ DevLs* dev_ls() {
               sym(lb, "cublasCreate_v2", d.cb_create) && sym(lb, "cublasSetStream_v2", d.cb_set_stream) &&
               sym(lb, "cublasDtrsm_v2", d.trsm) && sym(lb, "cublasDgemm_v2", d.gemm)))
             return;
+        if (sym(ls, "cusolverDnCreateGesvdjInfo", d.svdj_info) && sym(ls, "cusolverDnDgesvdj_bufferSize", d.svdj_ws) &&
+            sym(ls, "cusolverDnDgesvdj", d.svdj)) {
+            if (d.svdj_info(&d.svdj_params) != CUSOLVER_STATUS_SUCCESS) d.svdj = nullptr;
+        } else {
+            d.svdj = nullptr;
+        }
         if (cudaGetDevice(&d.device) != cudaSuccess) return;
         if (cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess) return;
         if (d.create(&d.sh) != CUSOLVER_STATUS_SUCCESS || d.set_stream(d.sh, d.stream) != CUSOLVER_STATUS_SUCCESS)
@@ -408,6 +419,63 @@ int device_tr_rse(const Cores& f, const Tensor& x, double* out) {
     }
     if (!(den > 0.0)) return -1;
     *out = std::sqrt(num) / std::sqrt(den);
+    return 0;
+}
+
+// Thin SVD a = U diag(s) V^T on the device (cuSOLVER gesvdj: one-sided Jacobi, as the host
+// stand-in for BDCSVD, solvers.hpp:297-334), s descending, then the host svd()'s conventions: the
+// left factor of the taller side zeroed where s_j = 0, and the shared sign rule (the entry of
+// largest magnitude of each U column positive). 0: done; -1: no device route (caller: host).
+int device_svd(const Mat& a, Mat& U, std::vector<double>& s, Mat& V) {
+    const idx m = a.r, n = a.c, k = std::min(m, n);
+    // below ~1e7 m n min(m, n) the host Jacobi is faster than the round trip
+    if (k < 1 || m > (1 << 30) || n > (1 << 30) || (double)m * (double)n * (double)k < 1e7) return -1;
+    std::lock_guard<std::mutex> lock(g_mu);
+    DevLs* d = dev_ls();
+    if (!d || !d->svdj) return -1;
+    cudaStream_t st = d->stream;
+    // A in dA, U in dS0, V in dS1, s in dtau
+    if (!grow(d->dA, d->capA, (size_t)(m * n)) || !grow(d->dS0, d->capS0, (size_t)(m * k)) ||
+        !grow(d->dS1, d->capS1, (size_t)(n * k)) || !grow(d->dtau, d->capT, (size_t)k))
+        return -1;
+    int lw = 0;
+    if (d->svdj_ws(d->sh, CUSOLVER_EIG_MODE_VECTOR, 1, (int)m, (int)n, d->dA, (int)m, d->dtau, d->dS0, (int)m, d->dS1,
+                   (int)n, &lw, d->svdj_params) != CUSOLVER_STATUS_SUCCESS ||
+        !grow(d->dwork, d->capW, (size_t)lw))
+        return -1;
+    if (cudaMemcpyAsync(d->dA, a.a.data(), sizeof(double) * m * n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return -1;
+    if (d->svdj(d->sh, CUSOLVER_EIG_MODE_VECTOR, 1, (int)m, (int)n, d->dA, (int)m, d->dtau, d->dS0, (int)m, d->dS1,
+                (int)n, d->dwork, (int)d->capW, d->dinfo, d->svdj_params) != CUSOLVER_STATUS_SUCCESS)
+        return -1;
+    Mat u(m, k), v(n, k);
+    std::vector<double> sv((size_t)k);
+    int info = 0;
+    if (cudaMemcpyAsync(u.a.data(), d->dS0, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(v.a.data(), d->dS1, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(sv.data(), d->dtau, sizeof(double) * k, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(&info, d->dinfo, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess || info != 0)
+        return -1;
+    for (idx j = 1; j < k; ++j)
+        if (sv[(size_t)j] > sv[(size_t)(j - 1)]) return -1;  // the contract is descending order
+    // host svd(): the columns of the taller side's factor are W(:, j) / s_j, zero when s_j = 0
+    Mat& tall = (m >= n) ? u : v;
+    for (idx j = 0; j < k; ++j)
+        if (!(sv[(size_t)j] > 0.0))
+            for (idx i = 0; i < tall.r; ++i) tall(i, j) = 0.0;
+    for (idx j = 0; j < k; ++j) {
+        idx arg = 0;
+        for (idx i = 1; i < u.r; ++i)
+            if (std::abs(u(i, j)) > std::abs(u(arg, j))) arg = i;
+        if (u(arg, j) < 0.0) {
+            for (idx i = 0; i < u.r; ++i) u(i, j) = -u(i, j);
+            for (idx i = 0; i < v.r; ++i) v(i, j) = -v(i, j);
+        }
+    }
+    U = std::move(u);
+    V = std::move(v);
+    s = std::move(sv);
     return 0;
 }
 

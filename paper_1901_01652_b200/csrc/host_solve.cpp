@@ -777,6 +777,7 @@ inline bool jacobi_rotate(double* wp, double* wq, double* vp, double* vq, idx m,
 }  // namespace
 
 void svd(const Mat& a, Mat& U, std::vector<double>& s, Mat& V) {
+    if (device_svd(a, U, s, V) == 0) return;  // large unfoldings (C5's 576 x 432) on the GPU
     const bool wide = a.r < a.c;
     Mat W = wide ? transpose(a) : a;
     const idx m = W.r, n = W.c;

@@ -70,6 +70,10 @@ int device_als_direct(const Cores& f, idx n, const Mat& xn_tr, Mat& z);
 // rse(x, reconstruct_full(f)) on the device (device_ls.cu). 0: *out set; -1: no device route.
 int device_tr_rse(const Cores& f, const Tensor& x, double* out);
 
+// Thin SVD on the device (cuSOLVER gesvdj) with the host svd()'s conventions (device_ls.cu).
+// 0: U (m x k), s (k, descending), V (n x k); -1: no device route.
+int device_svd(const Mat& a, Mat& U, std::vector<double>& s, Mat& V);
+
 // Phase timers of the small solve, on only with TRG_SOLVE_PROF=1 (printed to stderr after each
 // trals call; the device phases then synchronise after each step so the split is attributable).
 enum SolvePhase { kPhSubchain, kPhUnfold, kPhLsH2D, kPhLsFactor, kPhLsApply, kPhLsHost, kPhStore, kPhRse, kPhCount };
